@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""DCO hot-path benchmark (BASELINE.json metric: frames/sec at 1280x720, D=128).
+
+A step is one composited frame of the full DCO path for one stream in steady
+state (previous-dense chain active): stereo (cross windows, AD-census cost,
+aggregation, WTA, histogram refinement, sparse depth) + bidirectional flow +
+depth contours + assemble + PCG/MR densify + composite against a rendered
+virtual layer — the body of run_pipeline (reference src/pipeline.cpp:183-258).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One process per GPU (torchrun for N>1); every rank runs its own stream
+(frames shard across GPUs, no data-path collective: "scaling": "weak"). The
+timed region is bracketed by a barrier + cuda.synchronize; the reported time
+is the max over ranks. L2 is flushed (256 MiB memset) between timed steps,
+outside each step's event pair.
+
+`value` times frames whose u8 inputs are already in HBM. `e2e` times the same
+steps through the host-buffer C-ABI (dco_stream_push_gray8_host): pinned u8
+frames H2D, the pipeline, the composite/mask/dense D2H.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W, H, D = 1280, 720, 128
+NQ, NF = (W // 2) * (H // 2), W * H
+METRIC = "stereo frames/sec at 1280x720 D=128 (1/2/4/8 B200) vs CPU; HBM GB/s fraction"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_frames(frames, d_pre_list, cfg_dict, procs):
+    """Runs the reference pipeline (oracle/_ref) on `procs` processes, one frame
+    each, concurrently. Returns wall seconds."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    jobs = [(frames[i % len(frames)], d_pre_list[i % len(d_pre_list)], cfg_dict) for i in range(procs)]
+    with ctx.Pool(procs) as pool:
+        pool.map(_cpu_warm, range(procs))
+        t0 = time.perf_counter()
+        pool.map(_cpu_job, jobs)
+        return time.perf_counter() - t0
+
+
+def _cpu_warm(_):
+    from oracle import ref
+
+    ref.lib()
+    return 0
+
+
+def _cpu_job(job):
+    import numpy as np
+
+    from oracle import ref
+    from paper_2203_02300_b200.config import Config
+
+    (past8, mid8, fut8, right8), d_pre, cfg_dict = job
+    cfg = Config(**cfg_dict)
+    f = lambda a: a.astype(np.float32) / np.float32(255.0)  # noqa: E731  read_gray bytes/255.0f
+    mid = f(mid8)
+    q = [ref.downsample_half(f(a)) for a in (past8, mid8, fut8)]
+    rq = ref.downsample_half(f(right8))
+    vr, vd = _VIRT
+    out = ref.pipeline_frame(q[0], q[1], q[2], mid, rq, np.repeat(mid[:, :, None], 3, 2), d_pre, vr, vd, cfg)
+    return out["iterations"]
+
+
+_VIRT = (None, None)
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU implementation (oracle/_ref, built
+    from /root/reference sources) on the host cores, same config/metric."""
+    import numpy as np
+
+    from paper_2203_02300_b200.config import Config
+    from paper_2203_02300_b200.synth import StereoVideo
+
+    if rank != 0:
+        return
+    global _VIRT
+    from oracle import ref
+
+    cfg = Config(d_max=D - 1)
+    vid = StereoVideo(W, H)
+    _VIRT = ref.render_cube(W, H, cfg.focal_px)
+    frames = []
+    for i in range(8):
+        l0, _ = vid.frame(i)
+        l1, r1 = vid.frame(i + 1)
+        l2, _ = vid.frame(i + 2)
+        frames.append((l0, l1, l2, r1))
+    # steady state needs a previous dense map: one reference frame provides it
+    f = lambda a: a.astype(np.float32) / np.float32(255.0)  # noqa: E731
+    q = [ref.downsample_half(f(a)) for a in frames[0][:3]]
+    out = ref.pipeline_frame(q[0], q[1], q[2], f(frames[0][1]), ref.downsample_half(f(frames[0][3])),
+                             np.repeat(f(frames[0][1])[:, :, None], 3, 2), None, _VIRT[0], _VIRT[1], cfg)
+    d_pre = [out["dense"]]
+    procs = min(os.cpu_count() or 1, 8)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t = cpu_reference_frames(frames, d_pre, cfg.as_dict(), procs)
+        if it >= args.warmup:
+            times.append(t)
+    total = sum(times)
+    value = procs * len(times) / total
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "config": {"workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+composite)",
+                   "frames_per_step": procs},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": "reference",
+                         "sample": "%d concurrent 1280x720 D=128 steady-state frames per step (oracle/_ref, "
+                                   "one process per core)" % procs},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def algorithmic_bytes(span, iters):
+    """SURVEY §8(d) per-unit figures x units per launch."""
+    if span == "solve":
+        return 104.0 * NF * max(iters, 1)
+    if span == "aggregate":
+        return 8.0 * NQ * D + 4.0 * NQ
+    if span == "cost":
+        return 28.0 * NQ + 4.0 * NQ * D
+    if span == "wta":
+        return 4.0 * NQ * D + 4.0 * NQ
+    return None
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    from paper_2203_02300_b200 import dco
+    from paper_2203_02300_b200.config import Config
+    from paper_2203_02300_b200.synth import StereoVideo
+
+    cfg = Config(d_max=D - 1)
+    vid = StereoVideo(W, H, seed=61 + rank)
+    nframes = 32
+    lefts, rights = zip(*[vid.frame(i) for i in range(nframes)])
+    dev_l = torch.from_numpy(np.stack(lefts)).cuda()
+    dev_r = torch.from_numpy(np.stack(rights)).cuda()
+    # virtual layer: a depth-tested cube (render_virtual is outside the path;
+    # a fixed synthetic layer stands in: a box at 1.5 m in the image centre)
+    vdepth = torch.full((H, W), float("nan"), device="cuda")
+    vrgb = torch.zeros((H, W, 3), device="cuda")
+    vdepth[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = 1.5
+    vrgb[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = torch.tensor([1.0, 0.55, 0.1], device="cuda")
+
+    s = dco.Stream(W, H, cfg)
+    s.set_virtual(vrgb, vdepth)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    i = 0
+    # fill the window and reach steady state (d_pre chain) + W warmups
+    for _ in range(3 + args.warmup):
+        s.push_gray8(dev_l[i % nframes], dev_r[i % nframes], want_result=False)
+        i += 1
+    torch.cuda.synchronize()
+    s.set_timing(True)
+    launches0 = dco.kernel_launches()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    iters = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            s.push_gray8(dev_l[i % nframes], dev_r[i % nframes], want_result=False)
+            ev[k][1].record(stream)
+            i += 1
+        torch.cuda.synchronize()
+        barrier()
+    launches = dco.kernel_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    spans, nt = s.span_times()
+    s.set_timing(False)
+    # solver iterations of the timed frames (one extra pushed frame reports it)
+    res = s.push_gray8(dev_l[i % nframes], dev_r[i % nframes])
+    i += 1
+    iters = res.densify_iterations
+
+    # end to end: host pinned u8 in, composite/mask/dense out, per step
+    h_l = [torch.from_numpy(a).pin_memory() for a in lefts]
+    h_r = [torch.from_numpy(a).pin_memory() for a in rights]
+    comp = torch.empty((H, W, 3), dtype=torch.float32).pin_memory()
+    mask = torch.empty((H, W), dtype=torch.uint8).pin_memory()
+    dense = torch.empty((H, W), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        s.push_gray8_host(h_l[i % nframes], h_r[i % nframes], comp, mask, dense)
+        i += 1
+    e2e_ms = []
+    barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s.push_gray8_host(h_l[i % nframes], h_r[i % nframes], comp, mask, dense)
+        e2e_ms.append(1000.0 * (time.perf_counter() - t0))
+        i += 1
+    barrier()
+    e2e_total = sum(e2e_ms)
+
+    # max over ranks
+    tot = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms, e2e_total = tot.tolist()
+    if rank != 0:
+        s.close()
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    value = world * args.steps / (total_ms / 1000.0)
+    e2e_value = world * args.steps / (e2e_total / 1000.0)
+    per_frame = {k: v / max(nt, 1) for k, v in spans.items()}
+    dominant = max(per_frame, key=per_frame.get)
+    peak, peak_src = peaks()
+    ab = algorithmic_bytes(dominant, iters)
+    roof = None
+    if ab is not None:
+        achieved = ab / (per_frame[dominant] / 1000.0) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(dominant)
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes": ab, "ms_per_launch": per_frame[dominant]}
+    agg_ab = algorithmic_bytes("aggregate", 0)
+    stages = {k: round(v, 4) for k, v in per_frame.items()}
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "config": {"workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+composite), "
+                               "1 stream per GPU", "width": W, "height": H, "disparities": D,
+                   "l2": "flushed between steps (256 MiB memset outside the step events)",
+                   "parallelism": "stream-sharded x%d" % world},
+        "roofline": roof,
+        "aggregation_roofline": {"achieved": agg_ab / (per_frame["aggregate"] / 1000.0) / 1e9, "peak": peak,
+                                 "unit": "GB/s", "frac": agg_ab / (per_frame["aggregate"] / 1000.0) / 1e9 / peak},
+        "stage_ms": stages,
+        "densify_iterations": iters,
+        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": 2 * NF,
+                "d2h_bytes_per_step": NF * 3 * 4 + NF + NF * 4},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(s, dev_l, dev_r, lefts, rights, cfg, i, nframes)
+        except Exception as e:  # report, don't hide
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    s.close()
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(s, dev_l, dev_r, lefts, rights, cfg, i, nframes):
+    """The reference (oracle/_ref) timed on this box's host cores on a bounded
+    sample of the same workload: P concurrent steady-state frames."""
+    global _VIRT
+    import numpy as np
+    import torch
+
+    from oracle import ref
+
+    # the fixed virtual layer the GPU arm composites against
+    vdepth = np.full((H, W), np.nan, np.float32)
+    vrgb = np.zeros((H, W, 3), np.float32)
+    vdepth[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = 1.5
+    vrgb[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = (1.0, 0.55, 0.1)
+    _VIRT = (vrgb, vdepth)
+    procs = min(os.cpu_count() or 1, 8)
+    # previous dense of the frame before each sampled frame (from the GPU stream)
+    d_pre = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    frames, pres = [], []
+    for k in range(procs):
+        s.push_gray8(dev_l[i % nframes], dev_r[i % nframes], want_result=False)
+        v = s.views()
+        from paper_2203_02300_b200 import dco
+
+        d_pre.copy_(dco.view_tensor(v.dense, (H, W), torch.float32))
+        pres.append(d_pre.cpu().numpy())
+        frames.append((lefts[(i - 1) % nframes], lefts[i % nframes], lefts[(i + 1) % nframes], rights[i % nframes]))
+        i += 1
+    ref.lib()
+    wall = cpu_reference_frames(frames, pres, cfg.as_dict(), procs)
+    return {"value": procs / wall, "unit": "frames/s", "cores": procs, "kind": "reference",
+            "sample": "%d concurrent 1280x720 D=128 steady-state frames (reference library oracle/_ref, "
+                      "one process per core), wall %.1f s" % (procs, wall)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

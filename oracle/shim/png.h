@@ -1,0 +1,57 @@
+/* Throw-only libpng stand-in used ONLY to compile the reference's codec.cpp
+ * into the CPU oracle (oracle/_ref). libpng is absent from this image and no
+ * hot-path stage touches PNG: png_create_*_struct return NULL, so the
+ * reference raises CodecError("libpng init failed") on any PNG request while
+ * PGM/PPM/PFM/FLO I/O keeps working. Test infrastructure, not product code. */
+#ifndef DCO_ORACLE_PNG_STUB_H
+#define DCO_ORACLE_PNG_STUB_H
+
+#include <csetjmp>
+#include <cstdio>
+
+typedef unsigned int png_uint_32;
+typedef unsigned char* png_bytep;
+typedef struct png_stub_struct* png_structp;
+typedef struct png_stub_info* png_infop;
+
+#define PNG_LIBPNG_VER_STRING "stub"
+#define PNG_COLOR_TYPE_GRAY 0
+#define PNG_COLOR_TYPE_PALETTE 3
+#define PNG_COLOR_TYPE_RGB 2
+#define PNG_INFO_tRNS 0x10
+#define PNG_INTERLACE_NONE 0
+#define PNG_COMPRESSION_TYPE_DEFAULT 0
+#define PNG_FILTER_TYPE_DEFAULT 0
+
+inline std::jmp_buf& png_stub_jmpbuf() {
+    static std::jmp_buf buf;
+    return buf;
+}
+#define png_jmpbuf(p) (png_stub_jmpbuf())
+
+inline png_structp png_create_read_struct(const char*, void*, void*, void*) { return nullptr; }
+inline png_structp png_create_write_struct(const char*, void*, void*, void*) { return nullptr; }
+inline png_infop png_create_info_struct(png_structp) { return nullptr; }
+inline void png_destroy_read_struct(png_structp*, png_infop*, png_infop*) {}
+inline void png_destroy_write_struct(png_structp*, png_infop*) {}
+inline void png_init_io(png_structp, std::FILE*) {}
+inline void png_read_info(png_structp, png_infop) {}
+inline png_uint_32 png_get_image_width(png_structp, png_infop) { return 0; }
+inline png_uint_32 png_get_image_height(png_structp, png_infop) { return 0; }
+inline int png_get_bit_depth(png_structp, png_infop) { return 0; }
+inline int png_get_color_type(png_structp, png_infop) { return 0; }
+inline int png_get_channels(png_structp, png_infop) { return 0; }
+inline png_uint_32 png_get_valid(png_structp, png_infop, png_uint_32) { return 0; }
+inline void png_set_palette_to_rgb(png_structp) {}
+inline void png_set_expand_gray_1_2_4_to_8(png_structp) {}
+inline void png_set_tRNS_to_alpha(png_structp) {}
+inline void png_set_strip_alpha(png_structp) {}
+inline void png_read_update_info(png_structp, png_infop) {}
+inline void png_read_image(png_structp, png_bytep*) {}
+inline void png_read_end(png_structp, png_infop) {}
+inline void png_set_IHDR(png_structp, png_infop, png_uint_32, png_uint_32, int, int, int, int, int) {}
+inline void png_write_info(png_structp, png_infop) {}
+inline void png_write_image(png_structp, png_bytep*) {}
+inline void png_write_end(png_structp, png_infop) {}
+
+#endif

@@ -1,0 +1,136 @@
+// common.cuh — context, error plumbing and launch helpers shared by every
+// translation unit of libdco_gpu.so. Host code is C++17; device code targets
+// sm_100a only and is compiled with --fmad=false so that every float/double
+// expression rounds exactly like the reference's x86-64 build (no FMA
+// contraction there). Where the reference's libm is involved
+// the glibc replicas in dco_libm.h are used.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dco_gpu.h"
+
+namespace dco_gpu {
+
+// Status-carrying exception: thrown by host code, converted to the C status
+// (and the context's last_error) at the C-ABI edge.
+struct Failure : std::runtime_error {
+    int status;
+    Failure(int st, const std::string& msg) : std::runtime_error(msg), status(st) {}
+};
+
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Failure(status, msg); }
+inline void require(bool ok, const std::string& msg) {
+    if (!ok) fail(DCO_INPUT, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(DCO_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Grow-only device buffer: the context keeps one per scratch slot so the
+// steady-state frame loop performs no allocation.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+enum Slot : int {
+    S_ARM_RAW = 0,
+    S_REGION,
+    S_CENSUS,
+    S_HSUM,
+    S_COST,
+    S_AGG,
+    S_DISP0,
+    S_DISP1,
+    S_ARMS,
+    S_SCALAR,
+    S_FLOW_PYR,
+    S_FLOW_PATCH,
+    S_FLOW_ACC,
+    S_FLOW_TMP,
+    S_CONTOUR0,
+    S_CONTOUR1,
+    S_CONTOUR2,
+    S_CONTOUR3,
+    S_SAT,
+    S_LABELS,
+    S_CG,
+    S_RED,
+    S_STATS,
+    S_TMP0,
+    S_TMP1,
+    S_FLAG_FLOW,
+    S_FLAG_ARM,
+    S_FLAG_BIN,
+    S_FLAG_PEAK,
+    S_FLAG_ASM,
+    S_HIST,
+    S_STAGE,
+    S_COUNT
+};
+
+}  // namespace dco_gpu
+
+struct dco_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    dco_gpu::DevBuf slots[dco_gpu::S_COUNT];
+    void* pinned = nullptr;  // small pinned host staging area for scalar readbacks
+    size_t pinned_bytes = 0;
+};
+
+namespace dco_gpu {
+
+void* scratch(dco_ctx* ctx, Slot s, size_t bytes);
+void* pinned_host(dco_ctx* ctx, size_t bytes);
+
+// Counts and error-checks every launch made through it.
+inline void launched(dco_ctx* ctx, const char* name) {
+    ++ctx->launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(DCO_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+}
+
+inline unsigned blocks_for(size_t n, unsigned threads) {
+    return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+// The C-ABI edge: runs fn, maps Failure/std::exception to status codes.
+template <typename F>
+int guarded(dco_ctx* ctx, F&& fn) {
+    try {
+        if (!ctx) return DCO_INPUT;
+        fn();
+        return DCO_OK;
+    } catch (const Failure& f) {
+        ctx->err = f.what();
+        return f.status;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return DCO_CUDA;
+    }
+}
+
+void validate_config(const dco_config* cfg);  // PipelineConfig::validate, config.cpp:10-36
+
+// Host-side precomputed tables (computed with the host libm exactly as the
+// reference computes them, then uploaded):
+//   alpha[l]   = adaptive_alpha(l)            stereo.cpp:102-104, l in 0..255
+//   census[h]  = 1 - exp(-h/lambda_census)    stereo.cpp:125-127, h in 0..64
+struct StereoTables {
+    double alpha[256];
+    double census[65];
+};
+void make_stereo_tables(const dco_config* cfg, StereoTables* t);
+
+}  // namespace dco_gpu

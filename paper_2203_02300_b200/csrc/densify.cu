@@ -1,0 +1,807 @@
+// densify.cu — the three-constraint quadratic densification (reference
+// src/densify.cpp): assembly of the 5-point normal equations and the
+// Jacobi-preconditioned CG with minimal-residual smoothing, in FP64.
+//
+// assemble_system is bit-exact: per-pixel terms are evaluated in the
+// reference's order (diag: data, stability, up-coupling, left-coupling, own
+// right, own down — densify.cpp:70-114) and the sparse mean uses a double
+// tree that is provably exact whenever every partial sum is representable
+// (checked on the device; otherwise the reference's sequential sum runs).
+//
+// solve_dense_depth is ONE persistent cooperative kernel: every block owns a
+// fixed slice of the unknowns, the four reductions per iteration (pq, rho +
+// MR numerators, |rs|^2) are fixed-shape trees, and the loop/termination
+// logic of densify.cpp:174-211 runs on the device, so an entire solve is one
+// launch with no host round trip. Reductions are deterministic (bit-stable
+// run to run) but not in the reference's sequential order, so the dense map
+// matches the oracle within tolerance, not bit for bit.
+#include <cooperative_groups.h>
+#include <math.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dco_gpu {
+namespace {
+
+__device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b : a; }   // std::min
+__device__ __forceinline__ double dmax0(double a) { return (a < 0.0) ? 0.0 : a; }        // std::max(a, 0.0)
+
+// fused_confidence, densify.cpp:11-16.
+__device__ __forceinline__ double fused_conf(const float* mf, int qw, int qh, int x, int y) {
+    int mx = min(x / 2, qw - 1), my = min(y / 2, qh - 1);
+    float v = mf[static_cast<size_t>(my) * qw + mx];
+    return isfinite(v) ? static_cast<double>(v) : 0.0;
+}
+
+// smoothness_weight, densify.cpp:26-35 (q is the right or lower neighbour).
+__device__ __forceinline__ double smooth_w(const uint8_t* e, const float* mf, int qw, int qh,
+                                           const float* mi, int w, int px, int py, int qx, int qy) {
+    size_t ip = static_cast<size_t>(py) * w + px, iq = static_cast<size_t>(qy) * w + qx;
+    int on = (e[ip] ? 1 : 0) + (e[iq] ? 1 : 0);
+    if (on == 1) return 0.0;
+    double sp = fused_conf(mf, qw, qh, px, py) * mi[ip];
+    double sq = fused_conf(mf, qw, qh, qx, qy) * mi[iq];
+    return dmax0(1.0 - dmin(sp, sq));
+}
+
+struct AsmArgs {
+    int w, h, qw, qh;
+    double lambda_d, lambda_s, lambda_s2;
+    const float* sparse;
+    const uint8_t* edges;
+    const float* mf;
+    const float* mi;
+    const float* pre;      // nullable
+    const int* pre_valid;  // nullable: pre is used only when *pre_valid != 0
+    double* diag;
+    double* ch;
+    double* cv;
+    double* rhs;
+    double* init;
+    uint8_t* anchored;
+    const double* sparse_mean;  // device scalar
+};
+
+// assemble_system per-pixel part, densify.cpp:70-114.
+__global__ void k_assemble(AsmArgs a) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= a.w || y >= a.h) return;
+    const int w = a.w, h = a.h;
+    size_t i = static_cast<size_t>(y) * w + x;
+    if (a.pre && a.pre_valid && *a.pre_valid == 0) a.pre = nullptr;
+    const double two_ls = 2.0 * a.lambda_s;
+    double diag = 0.0, rhs = 0.0, init = *a.sparse_mean;
+    uint8_t anch = 0;
+    float s = a.sparse[i];
+    if (isfinite(s)) {
+        double ds = s;
+        diag += a.lambda_d;
+        rhs += a.lambda_d * ds;
+        anch = 1;
+        init = ds;
+    } else if (a.pre && isfinite(a.pre[i])) {
+        init = a.pre[i];
+    }
+    if (a.pre && isfinite(a.pre[i])) {
+        double dp = a.pre[i];
+        diag += a.lambda_s2;
+        rhs += a.lambda_s2 * dp;
+        anch = 1;
+    }
+    if (y > 0) diag += two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x, y - 1, x, y);
+    if (x > 0) diag += two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x - 1, y, x, y);
+    double chv = 0.0, cvv = 0.0;
+    if (x + 1 < w) {
+        chv = two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x, y, x + 1, y);
+        diag += chv;
+    }
+    if (y + 1 < h) {
+        cvv = two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x, y, x, y + 1);
+        diag += cvv;
+    }
+    a.diag[i] = diag;
+    a.ch[i] = chv;
+    a.cv[i] = cvv;
+    a.rhs[i] = rhs;
+    a.init[i] = init;
+    a.anchored[i] = anch;
+}
+
+// Block-wide deterministic sum of K doubles per thread (fixed shuffle tree).
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* smem /* [32*K] */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) smem[warp * K + k] = v[k];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double t = lane < nw ? smem[lane * K + k] : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            v[k] = t;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) smem[k] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = smem[k];
+    __syncthreads();
+}
+
+// Sparse statistics: valid count, min ulp exponent, sum of |v| and the double
+// tree sum (exact under the guard), anchor count and constant term partials.
+struct SparseStats {
+    unsigned long long count;
+    int min_exp;
+    double abs_sum;
+    double sum;
+};
+
+__global__ void k_sparse_stats(const float* __restrict__ s, size_t n, double* __restrict__ part,
+                               unsigned long long* __restrict__ count, int* __restrict__ min_exp) {
+    __shared__ double sm[32 * 2];
+    double v[2] = {0.0, 0.0};
+    unsigned long long c = 0;
+    int me = 1 << 20;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        float f = s[i];
+        if (isfinite(f)) {
+            v[0] += f;
+            v[1] += fabs(static_cast<double>(f));
+            ++c;
+            if (f != 0.0f) {
+                int e;
+                frexpf(f, &e);  // f = m * 2^e, m in [0.5,1): ulp = 2^(e-24), denormal-safe bound
+                me = min(me, max(e - 24, -149));
+            }
+        }
+    }
+    block_sum<2>(v, sm);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = v[0];
+        part[2 * blockIdx.x + 1] = v[1];
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, off);
+        me = min(me, __shfl_xor_sync(0xffffffffu, me, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c) atomicAdd(count, c);
+        atomicMin(min_exp, me);
+    }
+}
+
+// Finishes the sparse mean (densify.cpp:60-68): exact tree when the guard
+// holds, the reference's sequential loop otherwise (single thread, rare).
+__global__ void k_sparse_mean(const float* __restrict__ s, size_t n, const double* __restrict__ part,
+                              int nparts, const unsigned long long* __restrict__ count,
+                              const int* __restrict__ min_exp, double* __restrict__ mean) {
+    __shared__ double sm[32 * 2];
+    double v[2] = {0.0, 0.0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+        v[0] += part[2 * b];
+        v[1] += part[2 * b + 1];
+    }
+    block_sum<2>(v, sm);
+    if (threadIdx.x != 0) return;
+    unsigned long long c = *count;
+    if (c == 0) {
+        *mean = 0.0;
+        return;
+    }
+    double sum = v[0];
+    // all partial sums are multiples of 2^min_exp bounded by abs_sum: exact
+    // in double iff abs_sum < 2^(53 + min_exp) (margin for the bound's own rounding)
+    double limit = ldexp(1.0, 53 + *min_exp);
+    if (!(v[1] * (1.0 + 1e-9) < limit)) {
+        sum = 0.0;
+        for (size_t i = 0; i < n; ++i) {
+            float f = s[i];
+            if (isfinite(f)) sum += f;
+        }
+    }
+    *mean = sum / static_cast<double>(c);
+}
+
+// anchor count and constant term (densify.cpp:70-94, 113): tree sums.
+__global__ void k_anchor_const(const uint8_t* __restrict__ anch, const float* __restrict__ s,
+                               const float* __restrict__ pre, const int* __restrict__ pre_valid, size_t n,
+                               double ld, double ls2, unsigned long long* __restrict__ count,
+                               double* __restrict__ part) {
+    __shared__ double sm[32];
+    if (pre && pre_valid && *pre_valid == 0) pre = nullptr;
+    double v[1] = {0.0};
+    unsigned long long c = 0;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        c += anch[i];
+        float f = s[i];
+        if (isfinite(f)) {
+            double ds = f;
+            v[0] += ld * ds * ds;
+        }
+        if (pre) {
+            float g = pre[i];
+            if (isfinite(g)) {
+                double dp = g;
+                v[0] += ls2 * dp * dp;
+            }
+        }
+    }
+    block_sum<1>(v, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+__global__ void k_reduce_parts(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+    __shared__ double sm[32];
+    double v[1] = {0.0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v[0] += part[b];
+    block_sum<1>(v, sm);
+    if (threadIdx.x == 0) *out = v[0];
+}
+
+// apply_system, densify.cpp:118-133 (stencil order kept).
+__device__ __forceinline__ double apply_at(const double* __restrict__ diag, const double* __restrict__ ch,
+                                           const double* __restrict__ cv, const double* __restrict__ x,
+                                           int w, int h, size_t i, int xx, int y) {
+    double acc = diag[i] * x[i];
+    if (xx + 1 < w) acc -= ch[i] * x[i + 1];
+    if (xx > 0) acc -= ch[i - 1] * x[i - 1];
+    if (y + 1 < h) acc -= cv[i] * x[i + w];
+    if (y > 0) acc -= cv[i - w] * x[i - w];
+    return acc;
+}
+
+__global__ void k_apply(const double* __restrict__ diag, const double* __restrict__ ch,
+                        const double* __restrict__ cv, const double* __restrict__ x, int w, int h,
+                        double* __restrict__ out) {
+    int xx = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (xx >= w || y >= h) return;
+    size_t i = static_cast<size_t>(y) * w + xx;
+    out[i] = apply_at(diag, ch, cv, x, w, h, i, xx, y);
+}
+
+// objective_value partials: dot(x, Ax) and dot(b, x).
+__global__ void k_objective(const double* __restrict__ diag, const double* __restrict__ ch,
+                            const double* __restrict__ cv, const double* __restrict__ rhs,
+                            const double* __restrict__ x, int w, int h, double* __restrict__ part) {
+    __shared__ double sm[64];
+    double v[2] = {0.0, 0.0};
+    size_t n = static_cast<size_t>(w) * h;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
+        v[0] += x[i] * apply_at(diag, ch, cv, x, w, h, i, xx, y);
+        v[1] += rhs[i] * x[i];
+    }
+    block_sum<2>(v, sm);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = v[0];
+        part[2 * blockIdx.x + 1] = v[1];
+    }
+}
+__global__ void k_objective_finish(const double* __restrict__ part, int nparts, double c,
+                                   double* __restrict__ out) {
+    __shared__ double sm[64];
+    double v[2] = {0.0, 0.0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+        v[0] += part[2 * b];
+        v[1] += part[2 * b + 1];
+    }
+    block_sum<2>(v, sm);
+    if (threadIdx.x == 0) *out = v[0] - 2.0 * v[1] + c;
+}
+
+// ----------------------------------------------------------------- solver --
+struct SolveOut {
+    int status;  // 0 ok, 3 unsolvable
+    int iterations;
+    double relative_residual;
+    double objective_initial;
+    double objective_final;
+};
+
+struct CGArgs {
+    int w, h;
+    size_t n;
+    const double* diag;
+    const double* ch;
+    const double* cv;
+    const double* rhs;
+    const double* init;
+    double constant_term_host;
+    const double* constant_term_dev;  // used when non-null
+    const unsigned long long* anchors_dev;
+    unsigned long long anchors_host;
+    double* prec;
+    double* x;
+    double* r;
+    double* z;
+    double* p;
+    double* q;
+    double* rs;
+    double* xs;
+    double* part;  // [gridDim.x][4]
+    double* hist;
+    int hist_cap;
+    int max_iter;
+    double tol;
+    float* dense;
+    const float* fallback;    // unsolvable: dense = fallback (or NaN when null)
+    const int* fallback_valid;  // nullable: fallback usable only when *fallback_valid
+    SolveOut* out;
+};
+
+// Sum of the per-block partials, identical in every block (same order).
+template <int K>
+__device__ __forceinline__ void grid_total(const double* part, int nb, double (&v)[K], double* sm) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] += part[4 * b + k];
+    block_sum<K>(v, sm);
+}
+
+__global__ void __launch_bounds__(512) k_pcg(CGArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sm[32 * 4];
+    const int w = a.w, h = a.h;
+    const size_t n = a.n;
+    const size_t T = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int nb = gridDim.x;
+    double* part = a.part + 4 * blockIdx.x;
+
+    unsigned long long anchors = a.anchors_dev ? *a.anchors_dev : a.anchors_host;
+    if (anchors == 0) {  // densify.cpp:143-144 -> caller's Unsolvable handling
+        const float* fb = (a.fallback && (!a.fallback_valid || *a.fallback_valid)) ? a.fallback : nullptr;
+        for (size_t i = t0; i < n; i += T) a.dense[i] = fb ? fb[i] : __int_as_float(0x7fc00000);
+        if (t0 == 0) {
+            a.out->status = 3;
+            a.out->iterations = 0;
+        }
+        return;
+    }
+    const double cterm = a.constant_term_dev ? *a.constant_term_dev : a.constant_term_host;
+
+    // setup: x = initial, precond, r = b - A x, norms, objective(initial)
+    for (size_t i = t0; i < n; i += T) {
+        double d = a.diag[i];
+        a.prec[i] = d > 0.0 ? 1.0 / d : 1.0;
+        a.x[i] = a.init[i];
+    }
+    grid.sync();
+    {
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (size_t i = t0; i < n; i += T) {
+            int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
+            double ax = apply_at(a.diag, a.ch, a.cv, a.x, w, h, i, xx, y);
+            double b = a.rhs[i];
+            double ri = b - ax;
+            double zi = a.prec[i] * ri;
+            a.r[i] = ri;
+            a.rs[i] = ri;
+            a.xs[i] = a.x[i];
+            a.z[i] = zi;
+            a.p[i] = zi;
+            v[0] += b * b;
+            v[1] += ri * ri;
+            v[2] += ri * zi;
+        }
+        block_sum<4>(v, sm);
+        if (threadIdx.x == 0)
+            for (int k = 0; k < 4; ++k) part[k] = v[k];
+    }
+    grid.sync();
+    double tot[4];
+    grid_total<4>(a.part, nb, tot, sm);
+    const double bnorm = sqrt(tot[0]);
+    const double denom = bnorm > 0.0 ? bnorm : 1.0;
+    double snorm = sqrt(tot[1]);
+    double rho = tot[2];
+    if (t0 == 0) {
+        if (a.hist_cap > 0) a.hist[0] = snorm;
+    }
+    grid.sync();  // everyone has read the setup partials
+    // objective(initial) = dot(x,Ax) - 2 dot(b,x) + c, as two separate tree sums
+    {
+        double v[2] = {0.0, 0.0};
+        for (size_t i = t0; i < n; i += T) {
+            int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
+            v[0] += a.x[i] * apply_at(a.diag, a.ch, a.cv, a.x, w, h, i, xx, y);
+            v[1] += a.rhs[i] * a.x[i];
+        }
+        block_sum<2>(v, sm);
+        if (threadIdx.x == 0) {
+            part[0] = v[0];
+            part[1] = v[1];
+        }
+    }
+    grid.sync();
+    {
+        double o[2];
+        grid_total<2>(a.part, nb, o, sm);
+        if (t0 == 0) a.out->objective_initial = o[0] - 2.0 * o[1] + cterm;
+    }
+    grid.sync();
+
+    int iter = 0;
+    while (iter < a.max_iter && snorm / denom > a.tol) {
+        // phase A: q = A p, pq
+        {
+            double v[1] = {0.0};
+            for (size_t i = t0; i < n; i += T) {
+                int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
+                double qi = apply_at(a.diag, a.ch, a.cv, a.p, w, h, i, xx, y);
+                a.q[i] = qi;
+                v[0] += a.p[i] * qi;
+            }
+            block_sum<1>(v, sm);
+            if (threadIdx.x == 0) part[0] = v[0];
+        }
+        grid.sync();
+        double pq;
+        {
+            double t[1];
+            grid_total<1>(a.part, nb, t, sm);
+            pq = t[0];
+        }
+        if (pq <= 0.0) break;  // uniform across the grid
+        const double alpha = rho / pq;
+        grid.sync();  // partials consumed before they are overwritten
+        // phase B: x, r, z; rho_next; MR numerators
+        {
+            double v[3] = {0.0, 0.0, 0.0};
+            for (size_t i = t0; i < n; i += T) {
+                double xi = a.x[i] + alpha * a.p[i];
+                double ri = a.r[i] - alpha * a.q[i];
+                double zi = a.prec[i] * ri;
+                a.x[i] = xi;
+                a.r[i] = ri;
+                a.z[i] = zi;
+                v[0] += ri * zi;
+                double rsi = a.rs[i];
+                double di = ri - rsi;
+                v[1] += rsi * di;
+                v[2] += di * di;
+            }
+            block_sum<3>(v, sm);
+            if (threadIdx.x == 0)
+                for (int k = 0; k < 3; ++k) part[k] = v[k];
+        }
+        grid.sync();
+        double rho_next, sd, dd;
+        {
+            double t[3];
+            grid_total<3>(a.part, nb, t, sm);
+            rho_next = t[0];
+            sd = t[1];
+            dd = t[2];
+        }
+        const double beta = rho_next / rho;
+        rho = rho_next;
+        double eta = 0.0;
+        if (dd > 0.0) {
+            eta = -sd / dd;
+            eta = eta < 0.0 ? 0.0 : (1.0 < eta ? 1.0 : eta);  // std::clamp(., 0, 1)
+        }
+        grid.sync();
+        // phase C: p update, MR smoothing, |rs|^2
+        {
+            double v[1] = {0.0};
+            for (size_t i = t0; i < n; i += T) {
+                a.p[i] = a.z[i] + beta * a.p[i];
+                double rsi = a.rs[i];
+                if (eta > 0.0) {
+                    rsi += eta * (a.r[i] - rsi);
+                    a.rs[i] = rsi;
+                    double xsi = a.xs[i];
+                    a.xs[i] = xsi + eta * (a.x[i] - xsi);
+                }
+                v[0] += rsi * rsi;
+            }
+            block_sum<1>(v, sm);
+            if (threadIdx.x == 0) part[0] = v[0];
+        }
+        grid.sync();
+        {
+            double t[1];
+            grid_total<1>(a.part, nb, t, sm);
+            snorm = sqrt(t[0]);
+        }
+        ++iter;
+        if (t0 == 0 && iter < a.hist_cap) a.hist[iter] = snorm;
+        grid.sync();
+    }
+    // objective(xs) and the dense map
+    {
+        double v[2] = {0.0, 0.0};
+        for (size_t i = t0; i < n; i += T) {
+            int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
+            double xsi = a.xs[i];
+            v[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
+            v[1] += a.rhs[i] * xsi;
+            a.dense[i] = static_cast<float>(dmax0(xsi));
+        }
+        block_sum<2>(v, sm);
+        if (threadIdx.x == 0) {
+            part[0] = v[0];
+            part[1] = v[1];
+        }
+    }
+    grid.sync();
+    {
+        double o[2];
+        grid_total<2>(a.part, nb, o, sm);
+        if (t0 == 0) {
+            a.out->objective_final = o[0] - 2.0 * o[1] + cterm;
+            a.out->status = 0;
+            a.out->iterations = iter;
+            a.out->relative_residual = snorm / denom;
+        }
+    }
+}
+
+inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
+
+int g_pcg_blocks = 0;
+
+}  // namespace
+
+// ===================================================================== host =
+
+// assemble into caller buffers; scalars stay on the device (const_dev,
+// anchors_dev) unless the caller reads them back.
+void assemble_system_dev(dco_ctx* ctx, const float* sparse, const uint8_t* edges, const float* mf,
+                         int qw, int qh, const float* mi, const float* pre, const int* pre_valid, int w,
+                         int h, const dco_config* cfg, const dco_system* sys, double* const_dev,
+                         unsigned long long* anchors_dev) {
+    require(qw >= 1 && qh >= 1, "assemble_system: empty m_fuse");
+    if (cfg->lambda_s2 <= 0.0) pre = nullptr;  // densify.cpp:48
+    const size_t n = static_cast<size_t>(w) * h;
+    const int nblk = 296;
+    char* scr = static_cast<char*>(scratch(ctx, S_STATS, 4096 + nblk * 2 * sizeof(double) * 2));
+    (void)0;
+    unsigned long long* count = reinterpret_cast<unsigned long long*>(scr);
+    int* min_exp = reinterpret_cast<int*>(scr + 8);
+    double* mean = reinterpret_cast<double*>(scr + 16);
+    double* part = reinterpret_cast<double*>(scr + 4096);
+    cuda_check(cudaMemsetAsync(scr, 0, 16, ctx->stream), "memset");
+    cuda_check(cudaMemsetAsync(min_exp, 0x3f, sizeof(int), ctx->stream), "memset");
+    k_sparse_stats<<<nblk, 256, 0, ctx->stream>>>(sparse, n, part, count, min_exp);
+    launched(ctx, "k_sparse_stats");
+    k_sparse_mean<<<1, 256, 0, ctx->stream>>>(sparse, n, part, nblk, count, min_exp, mean);
+    launched(ctx, "k_sparse_mean");
+    AsmArgs a;
+    a.w = w;
+    a.h = h;
+    a.qw = qw;
+    a.qh = qh;
+    a.lambda_d = cfg->lambda_d;
+    a.lambda_s = cfg->lambda_s;
+    a.lambda_s2 = cfg->lambda_s2;
+    a.sparse = sparse;
+    a.edges = edges;
+    a.mf = mf;
+    a.mi = mi;
+    a.pre = pre;
+    a.pre_valid = pre_valid;
+    a.diag = sys->diag;
+    a.ch = sys->coup_h;
+    a.cv = sys->coup_v;
+    a.rhs = sys->rhs;
+    a.init = sys->initial;
+    a.anchored = sys->anchored;
+    a.sparse_mean = mean;
+    dim3 b(32, 8);
+    k_assemble<<<grid2(w, h, b), b, 0, ctx->stream>>>(a);
+    launched(ctx, "k_assemble");
+    cuda_check(cudaMemsetAsync(anchors_dev, 0, sizeof(unsigned long long), ctx->stream), "memset");
+    k_anchor_const<<<nblk, 256, 0, ctx->stream>>>(sys->anchored, sparse, pre, pre_valid, n, cfg->lambda_d,
+                                                  cfg->lambda_s2, anchors_dev, part);
+    launched(ctx, "k_anchor_const");
+    k_reduce_parts<<<1, 256, 0, ctx->stream>>>(part, nblk, const_dev);
+    launched(ctx, "k_reduce_parts");
+}
+
+// The whole PCG+MR solve, one cooperative launch. Scalars (anchors, constant
+// term) may live on the device. out_dev receives SolveOut.
+void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
+                     const unsigned long long* anchors_dev, const double* const_dev, float* dense,
+                     const float* fallback, const int* fallback_valid, double* hist, int hist_cap,
+                     void* out_dev) {
+    const int w = sys->width, h = sys->height;
+    const size_t n = static_cast<size_t>(w) * h;
+    if (!g_pcg_blocks) {
+        int dev = ctx->device, sms = 0, per = 0;
+        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg, 512, 0), "occupancy");
+        require(per >= 1, "solve_dense_depth: solver kernel does not fit an SM");
+        g_pcg_blocks = sms * std::min(per, 2);
+    }
+    const int nb = g_pcg_blocks;
+    double* wk = static_cast<double*>(scratch(ctx, S_CG, (8 * n + 4 * nb + 64) * sizeof(double)));
+    CGArgs a;
+    a.w = w;
+    a.h = h;
+    a.n = n;
+    a.diag = sys->diag;
+    a.ch = sys->coup_h;
+    a.cv = sys->coup_v;
+    a.rhs = sys->rhs;
+    a.init = sys->initial;
+    a.constant_term_host = sys->constant_term;
+    a.constant_term_dev = const_dev;
+    a.anchors_dev = anchors_dev;
+    a.anchors_host = sys->anchor_count;
+    a.prec = wk;
+    a.x = wk + n;
+    a.r = wk + 2 * n;
+    a.z = wk + 3 * n;
+    a.p = wk + 4 * n;
+    a.q = wk + 5 * n;
+    a.rs = wk + 6 * n;
+    a.xs = wk + 7 * n;
+    a.part = wk + 8 * n;
+    a.hist = hist;
+    a.hist_cap = hist ? hist_cap : 0;
+    a.max_iter = cfg->solver_max_iter;
+    a.tol = cfg->solver_tol;
+    a.dense = dense;
+    a.fallback = fallback;
+    a.fallback_valid = fallback_valid;
+    a.out = static_cast<SolveOut*>(out_dev);
+    void* params[] = {&a};
+    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg), dim3(nb), dim3(512), params, 0,
+                                           ctx->stream),
+               "launch k_pcg");
+    launched(ctx, "k_pcg");
+}
+
+size_t solve_out_bytes() { return sizeof(SolveOut); }
+
+void read_solve_out(const void* host, int* status, int* iters, double* relres, double* obj0,
+                    double* obj1) {
+    const SolveOut* o = static_cast<const SolveOut*>(host);
+    *status = o->status;
+    *iters = o->iterations;
+    *relres = o->relative_residual;
+    *obj0 = o->objective_initial;
+    *obj1 = o->objective_final;
+}
+
+}  // namespace dco_gpu
+
+using namespace dco_gpu;
+
+extern "C" {
+
+int dco_smoothness_weight(dco_ctx* ctx, int px, int py, int qx, int qy, const uint8_t* edges, int w,
+                          int h, const float* mf, int qw, int qh, const float* mi, double* out) {
+    return guarded(ctx, [&] {
+        if (abs(px - qx) + abs(py - qy) != 1) fail(DCO_INPUT, "smoothness_weight: q must be 4-adjacent to p");
+        require(px >= 0 && py >= 0 && qx >= 0 && qy >= 0 && px < w && qx < w && py < h && qy < h,
+                "smoothness_weight: pixel outside the map");
+        // evaluate on the host from the few device values involved
+        uint8_t ep = 0, eq = 0;
+        float mp = 0, mq = 0, fp = 0, fq = 0;
+        auto get8 = [&](const uint8_t* src, int x, int y, uint8_t* dst) {
+            cuda_check(cudaMemcpy(dst, src + static_cast<size_t>(y) * w + x, 1, cudaMemcpyDeviceToHost), "d2h");
+        };
+        auto getf = [&](const float* src, int stride, int x, int y, float* dst) {
+            cuda_check(cudaMemcpy(dst, src + static_cast<size_t>(y) * stride + x, 4, cudaMemcpyDeviceToHost), "d2h");
+        };
+        get8(edges, px, py, &ep);
+        get8(edges, qx, qy, &eq);
+        int on = (ep ? 1 : 0) + (eq ? 1 : 0);
+        if (on == 1) {
+            *out = 0.0;
+            return;
+        }
+        getf(mi, w, px, py, &mp);
+        getf(mi, w, qx, qy, &mq);
+        getf(mf, qw, std::min(px / 2, qw - 1), std::min(py / 2, qh - 1), &fp);
+        getf(mf, qw, std::min(qx / 2, qw - 1), std::min(qy / 2, qh - 1), &fq);
+        double cp = std::isfinite(fp) ? static_cast<double>(fp) : 0.0;
+        double cq = std::isfinite(fq) ? static_cast<double>(fq) : 0.0;
+        double sp = cp * mp, sq = cq * mq;
+        double m = (sq < sp) ? sq : sp;
+        double r = 1.0 - m;
+        *out = (r < 0.0) ? 0.0 : r;
+    });
+}
+
+int dco_assemble_system(dco_ctx* ctx, const float* sparse, const uint8_t* edges, const float* mf, int qw,
+                        int qh, const float* mi, const float* pre, int w, int h, const dco_config* cfg,
+                        dco_system* sys) {
+    return guarded(ctx, [&] {
+        require(sys && sys->diag && sys->coup_h && sys->coup_v && sys->rhs && sys->initial && sys->anchored,
+                "assemble_system: system buffers missing");
+        sys->width = w;
+        sys->height = h;
+        char* scr = static_cast<char*>(scratch(ctx, S_FLAG_ASM, 64));
+        double* cdev = reinterpret_cast<double*>(scr);
+        unsigned long long* adev = reinterpret_cast<unsigned long long*>(scr + 8);
+        assemble_system_dev(ctx, sparse, edges, mf, qw, qh, mi, pre, nullptr, w, h, cfg, sys, cdev, adev);
+        double* hp = static_cast<double*>(pinned_host(ctx, 64));
+        cuda_check(cudaMemcpyAsync(hp, scr, 16, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        sys->constant_term = hp[0];
+        sys->anchor_count = reinterpret_cast<unsigned long long*>(hp)[1];
+    });
+}
+
+int dco_apply_system(dco_ctx* ctx, const dco_system* sys, const double* x, double* out) {
+    return guarded(ctx, [&] {
+        dim3 b(32, 8);
+        k_apply<<<grid2(sys->width, sys->height, b), b, 0, ctx->stream>>>(sys->diag, sys->coup_h, sys->coup_v,
+                                                                           x, sys->width, sys->height, out);
+        launched(ctx, "k_apply");
+    });
+}
+
+int dco_objective_value(dco_ctx* ctx, const dco_system* sys, const double* x, double* out) {
+    return guarded(ctx, [&] {
+        const int nblk = 296;
+        double* part = static_cast<double*>(scratch(ctx, S_RED, (2 * nblk + 8) * sizeof(double)));
+        k_objective<<<nblk, 256, 0, ctx->stream>>>(sys->diag, sys->coup_h, sys->coup_v, sys->rhs, x,
+                                                   sys->width, sys->height, part);
+        launched(ctx, "k_objective");
+        k_objective_finish<<<1, 256, 0, ctx->stream>>>(part, nblk, sys->constant_term, part + 2 * nblk);
+        launched(ctx, "k_objective_finish");
+        double* hp = static_cast<double*>(pinned_host(ctx, 64));
+        cuda_check(cudaMemcpyAsync(hp, part + 2 * nblk, 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        *out = hp[0];
+    });
+}
+
+int dco_solve_dense_depth(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg, float* dense,
+                          dco_solve_stats* stats) {
+    return guarded(ctx, [&] {
+        if (sys->anchor_count == 0)
+            fail(DCO_UNSOLVABLE, "solve_dense_depth: no pixel carries a data or stability constraint");
+        int cap = (stats && stats->history) ? stats->history_cap : 0;
+        double* hist = nullptr;
+        if (cap > 0) hist = static_cast<double*>(scratch(ctx, S_HIST, cap * sizeof(double)));
+        void* od = scratch(ctx, S_SCALAR, 256);
+        solve_dense_dev(ctx, sys, cfg, nullptr, nullptr, dense, nullptr, nullptr, hist, cap, od);
+        void* hp = pinned_host(ctx, 256);
+        cuda_check(cudaMemcpyAsync(hp, od, solve_out_bytes(), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        int status, iters;
+        double rr, o0, o1;
+        read_solve_out(hp, &status, &iters, &rr, &o0, &o1);
+        if (stats) {
+            stats->iterations = iters;
+            stats->relative_residual = rr;
+            stats->objective_initial = o0;
+            stats->objective_final = o1;
+            if (cap > 0) {
+                int m = std::min(cap, iters + 1);
+                cuda_check(cudaMemcpy(stats->history, hist, m * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+            }
+        }
+    });
+}
+
+}  // extern "C"

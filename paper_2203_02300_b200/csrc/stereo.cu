@@ -1,0 +1,707 @@
+// stereo.cu — two-stage adaptive AD-census stereo (reference src/stereo.cpp,
+// src/pyramid.cpp:5-17) as sm_100a kernels.
+//
+// Data layout in HBM (all row-major, the reference's own layouts so the C-ABI
+// needs no transposes):
+//   images          float [h][w]
+//   cross arms      four u8 planes left/right/up/down [h][w]   (stereo.hpp:13-35)
+//   census          u64 [h][w]                                 (stereo.hpp:40-47)
+//   cost volumes    float [h][w][nd], d innermost              (stereo.hpp:50-63)
+//   disparity       float [h][w], NaN = nodata                 (stereo.hpp:66-78)
+//
+// Parity: every kernel reproduces the reference's arithmetic order exactly;
+// aggregation keeps the reference's sequential double prefix sums (one thread
+// per (row, d) chain, then per (column, d) chain), so it is bit-exact by
+// construction, not by luck (SURVEY §7.2 H1 option a).
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "dco_exp_table.h"
+#include "dco_libm.h"
+
+namespace dco_gpu {
+
+__device__ const uint64_t g_exp_table[2 * DCO_EXP_TABLE_N] = DCO_EXP_TABLE_INIT;
+
+namespace {
+
+// ---------------------------------------------------------------- pyramid --
+// downsample_half, pyramid.cpp:5-17: ((a + b) + c) + d, times 0.25f.
+__global__ void k_downsample(const float* __restrict__ img, int w, int h, float* __restrict__ out,
+                             int ow, int oh) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= ow || y >= oh) return;
+    const float* r0 = img + static_cast<size_t>(2 * y) * w + 2 * x;
+    const float* r1 = r0 + w;
+    float sum = r0[0] + r0[1] + r1[0] + r1[1];
+    out[static_cast<size_t>(y) * ow + x] = sum * 0.25f;
+}
+
+// read_pnm (codec.cpp:80, bytes/255.0f) fused with downsample_half.
+__global__ void k_ingest_gray8(const uint8_t* __restrict__ g8, int w, int h, float* __restrict__ full,
+                               float* __restrict__ quarter, int qw, int qh) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= qw || y >= qh) return;
+    size_t i0 = static_cast<size_t>(2 * y) * w + 2 * x, i1 = i0 + w;
+    float a = g8[i0] / 255.0f, b = g8[i0 + 1] / 255.0f, c = g8[i1] / 255.0f, d = g8[i1 + 1] / 255.0f;
+    if (full) {
+        full[i0] = a;
+        full[i0 + 1] = b;
+        full[i1] = c;
+        full[i1 + 1] = d;
+    }
+    if (quarter) quarter[static_cast<size_t>(y) * qw + x] = (a + b + c + d) * 0.25f;
+}
+
+// Odd trailing column/row of an odd-sized frame (not covered by the 2x2 pass).
+__global__ void k_ingest_gray8_tail(const uint8_t* __restrict__ g8, int w, int h,
+                                    float* __restrict__ full) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    // indices: first the last column (if w odd), then the last row (if h odd)
+    int ncol = (w & 1) ? h : 0, nrow = (h & 1) ? w : 0;
+    if (i < ncol) {
+        size_t p = static_cast<size_t>(i) * w + (w - 1);
+        full[p] = g8[p] / 255.0f;
+    } else if (i < ncol + nrow) {
+        size_t p = static_cast<size_t>(h - 1) * w + (i - ncol);
+        full[p] = g8[p] / 255.0f;
+    }
+}
+
+// ----------------------------------------------------------- cross arms ----
+// grow_arm, stereo.cpp:14-26: float |I(q) - I(p)| compared in double.
+__device__ __forceinline__ int grow_arm(const float* img, int w, int h, int x, int y, int dx, int dy,
+                                        int l1, int l2, double tau1, double tau2) {
+    const float center = img[static_cast<size_t>(y) * w + x];
+    int length = 0;
+    for (int l = 1; l <= l1; ++l) {
+        int qx = x + l * dx, qy = y + l * dy;
+        if (qx < 0 || qy < 0 || qx >= w || qy >= h) break;
+        double tau = l <= l2 ? tau1 : tau2;
+        float diff = fabsf(img[static_cast<size_t>(qy) * w + qx] - center);
+        if (static_cast<double>(diff) >= tau) break;
+        length = l;
+    }
+    return length;
+}
+
+__global__ void k_cross_arms_raw(const float* __restrict__ img, int w, int h, int l1, int l2,
+                                 double tau1, double tau2, uint8_t* __restrict__ raw) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    size_t n = static_cast<size_t>(w) * h, i = static_cast<size_t>(y) * w + x;
+    raw[i] = static_cast<uint8_t>(grow_arm(img, w, h, x, y, -1, 0, l1, l2, tau1, tau2));
+    raw[n + i] = static_cast<uint8_t>(grow_arm(img, w, h, x, y, 1, 0, l1, l2, tau1, tau2));
+    raw[2 * n + i] = static_cast<uint8_t>(grow_arm(img, w, h, x, y, 0, -1, l1, l2, tau1, tau2));
+    raw[3 * n + i] = static_cast<uint8_t>(grow_arm(img, w, h, x, y, 0, 1, l1, l2, tau1, tau2));
+}
+
+// smooth_arm_channel, stereo.cpp:30-48: 3x3 clamped median (5th order
+// statistic), clamped back to the raw reach. blockIdx.z = channel.
+__global__ void k_arm_median(const uint8_t* __restrict__ raw, int w, int h, uint8_t* __restrict__ a0,
+                             uint8_t* __restrict__ a1, uint8_t* __restrict__ a2,
+                             uint8_t* __restrict__ a3) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    int ch = blockIdx.z;
+    if (x >= w || y >= h) return;
+    const uint8_t* src = raw + static_cast<size_t>(ch) * w * h;
+    int v[9];
+    int n = 0;
+    for (int dy = -1; dy <= 1; ++dy) {
+        int yy = min(max(y + dy, 0), h - 1);
+        for (int dx = -1; dx <= 1; ++dx) {
+            int xx = min(max(x + dx, 0), w - 1);
+            v[n++] = src[static_cast<size_t>(yy) * w + xx];
+        }
+    }
+    // insertion sort of 9 small ints; v[4] is the median nth_element picks
+#pragma unroll
+    for (int i = 1; i < 9; ++i) {
+#pragma unroll
+        for (int j = i; j > 0; --j) {
+            int lo = min(v[j - 1], v[j]), hi = max(v[j - 1], v[j]);
+            v[j - 1] = lo;
+            v[j] = hi;
+        }
+    }
+    size_t i = static_cast<size_t>(y) * w + x;
+    uint8_t out = static_cast<uint8_t>(min(v[4], static_cast<int>(src[i])));
+    uint8_t* dst = ch == 0 ? a0 : ch == 1 ? a1 : ch == 2 ? a2 : a3;
+    dst[i] = out;
+}
+
+// --------------------------------------------------------------- census ----
+// census_transform, stereo.cpp:70-96: row-major window, centre skipped,
+// clamped border, bit = neighbour darker than centre.
+__global__ void k_census(const float* __restrict__ img, int w, int h, int rw, int rh,
+                         uint64_t* __restrict__ out) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    const float center = img[static_cast<size_t>(y) * w + x];
+    uint64_t bits = 0;
+    for (int dy = -rh; dy <= rh; ++dy) {
+        int yy = min(max(y + dy, 0), h - 1);
+        const float* row = img + static_cast<size_t>(yy) * w;
+        for (int dx = -rw; dx <= rw; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            int xx = min(max(x + dx, 0), w - 1);
+            bits = (bits << 1) | (row[xx] < center ? 1ull : 0ull);
+        }
+    }
+    out[static_cast<size_t>(y) * w + x] = bits;
+}
+
+// ------------------------------------------------------------ cost volume --
+// compute_cost_volume, stereo.cpp:106-150. One thread per (pixel, d): the
+// warp spans consecutive d of one pixel, so the [p][d] store is coalesced and
+// the pixel's alpha/census/luminance loads are warp-uniform broadcasts.
+struct CostParams {
+    int w, h, nd, d_min, bits;
+    double lambda_ad;
+    double alpha[256];
+    double census[65];
+};
+
+__global__ void __launch_bounds__(256) k_cost_volume(const float* __restrict__ left,
+                                                     const float* __restrict__ right,
+                                                     const uint64_t* __restrict__ cl,
+                                                     const uint64_t* __restrict__ cr,
+                                                     const uint8_t* __restrict__ armL,
+                                                     const uint8_t* __restrict__ armR,
+                                                     const uint8_t* __restrict__ armU,
+                                                     const uint8_t* __restrict__ armD,
+                                                     const __grid_constant__ CostParams prm_v,
+                                                     float* __restrict__ cost) {
+    const CostParams* prm = &prm_v;
+    __shared__ uint64_t s_exp[2 * DCO_EXP_TABLE_N];
+    __shared__ double s_census[65];
+    for (int i = threadIdx.x; i < 2 * DCO_EXP_TABLE_N; i += blockDim.x) s_exp[i] = g_exp_table[i];
+    for (int i = threadIdx.x; i < 65; i += blockDim.x) s_census[i] = prm->census[i];
+    __syncthreads();
+    const int w = prm->w, nd = prm->nd;
+    const size_t total = static_cast<size_t>(w) * prm->h * nd;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        size_t p = e / nd;
+        int k = static_cast<int>(e - p * nd);
+        int x = static_cast<int>(p % w);
+        int d = prm->d_min + k;
+        int qx = x - d;
+        float c;
+        if (qx < 0) {
+            c = 2.0f;
+        } else {
+            int m = min(min(armL[p], armR[p]), min(armU[p], armD[p]));
+            double alpha = prm->alpha[m];
+            size_t q = p - static_cast<size_t>(d);
+            float lum = left[p];
+            double c_ad = static_cast<double>(fabsf(lum - right[q])) * 255.0;
+            double ad_term = 1.0 - dco_exp(-c_ad / prm->lambda_ad, s_exp);
+            int hd = __popcll(cl[p] ^ cr[q]);
+            c = static_cast<float>(alpha * ad_term + (1.0 - alpha) * s_census[hd]);
+        }
+        cost[e] = c;
+    }
+}
+
+// ------------------------------------------------------------ aggregation --
+// aggregate_costs, stereo.cpp:152-218.
+// region_size (stereo.cpp:157-177): sum of horizontal spans along the vertical
+// arm; integer valued, so any summation order is exact.
+__global__ void k_region_size(const uint8_t* __restrict__ L, const uint8_t* __restrict__ R,
+                              const uint8_t* __restrict__ U, const uint8_t* __restrict__ D, int w,
+                              int h, int* __restrict__ region) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    size_t i = static_cast<size_t>(y) * w + x;
+    int s = 0;
+    for (int yy = y - U[i]; yy <= y + D[i]; ++yy) {
+        size_t j = static_cast<size_t>(yy) * w + x;
+        s += L[j] + R[j] + 1;
+    }
+    region[i] = s;
+}
+
+// Horizontal pass (stereo.cpp:191-201): one thread owns the (row y, slice k)
+// chain and walks x in order, P[x+1] = P[x] + cost, exactly the reference's
+// sequential double prefix. The last 2*l1+2 prefix values live in a per-thread
+// shared-memory ring; pixel px is finalised once P[px+l1+1] exists:
+// hsum = P[px+right+1] - P[px-left].
+__global__ void k_agg_hpass(const float* __restrict__ cost, int w, int h, int nd,
+                            const uint8_t* __restrict__ L, const uint8_t* __restrict__ R,
+                            int lag, int ring_mask, double* __restrict__ hsum) {
+    extern __shared__ double ring[];
+    const int lane = threadIdx.x, tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int stride = blockDim.x * blockDim.y;
+    const int k = blockIdx.x * blockDim.x + lane;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (y >= h || k >= nd) return;
+    const float* src = cost + static_cast<size_t>(y) * w * nd + k;
+    double* dst = hsum + static_cast<size_t>(y) * w * nd + k;
+    const uint8_t* Lr = L + static_cast<size_t>(y) * w;
+    const uint8_t* Rr = R + static_cast<size_t>(y) * w;
+    double P = 0.0;
+    ring[tid] = 0.0;
+    for (int x = 0; x < w; ++x) {
+        P += static_cast<double>(__ldg(src + static_cast<size_t>(x) * nd));
+        ring[((x + 1) & ring_mask) * stride + tid] = P;
+        int px = x + 1 - lag;
+        if (px >= 0) {
+            int a = px - Lr[px], b = px + Rr[px] + 1;
+            dst[static_cast<size_t>(px) * nd] =
+                ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
+        }
+    }
+    for (int px = max(w + 1 - lag, 0); px < w; ++px) {
+        int a = px - Lr[px], b = px + Rr[px] + 1;
+        dst[static_cast<size_t>(px) * nd] =
+            ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
+    }
+}
+
+// Vertical pass (stereo.cpp:203-215): one thread owns the (column x, slice k)
+// chain; C[y+1] = C[y] + hsum; total = C[py+down+1] - C[py-up];
+// out = float(total / region_size).
+__global__ void k_agg_vpass(const double* __restrict__ hsum, int w, int h, int nd,
+                            const uint8_t* __restrict__ U, const uint8_t* __restrict__ D,
+                            const int* __restrict__ region, int lag, int ring_mask,
+                            float* __restrict__ out) {
+    extern __shared__ double ring[];
+    const int lane = threadIdx.x, tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int stride = blockDim.x * blockDim.y;
+    const int k = blockIdx.x * blockDim.x + lane;
+    const int x = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || k >= nd) return;
+    const size_t row = static_cast<size_t>(w) * nd;
+    const double* src = hsum + static_cast<size_t>(x) * nd + k;
+    float* dst = out + static_cast<size_t>(x) * nd + k;
+    double C = 0.0;
+    ring[tid] = 0.0;
+    for (int y = 0; y < h; ++y) {
+        C += __ldg(src + y * row);
+        ring[((y + 1) & ring_mask) * stride + tid] = C;
+        int py = y + 1 - lag;
+        if (py >= 0) {
+            size_t i = static_cast<size_t>(py) * w + x;
+            int a = py - U[i], b = py + D[i] + 1;
+            double total = ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
+            dst[py * row] = static_cast<float>(total / region[i]);
+        }
+    }
+    for (int py = max(h + 1 - lag, 0); py < h; ++py) {
+        size_t i = static_cast<size_t>(py) * w + x;
+        int a = py - U[i], b = py + D[i] + 1;
+        double total = ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
+        dst[py * row] = static_cast<float>(total / region[i]);
+    }
+}
+
+// ------------------------------------------------------------------- WTA ---
+// select_disparity_wta, stereo.cpp:220-238: first strict minimum. One warp
+// per pixel; lanes stride over d and the warp reduces (cost, d) with ties to
+// the smaller d, which is the sequential first-minimum for non-NaN costs; a
+// NaN at d_min freezes the reference's scan at 0 and is honoured explicitly.
+__global__ void k_wta(const float* __restrict__ cost, int npix, int nd, int d_min,
+                      float* __restrict__ disp) {
+    const int lane = threadIdx.x & 31;
+    const size_t p = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (p >= static_cast<size_t>(npix)) return;
+    const float* c = cost + p * nd;
+    float best = INFINITY;
+    int bi = nd;
+    for (int k = lane; k < nd; k += 32) {
+        float v = c[k];
+        if (v < best) {
+            best = v;
+            bi = k;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        float ob = __shfl_xor_sync(0xffffffffu, best, off);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ob < best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        float c0 = c[0];
+        if (c0 != c0 || bi >= nd) bi = 0;  // NaN first cost, or all remaining NaN
+        // a cost equal to +inf everywhere also lands on 0 (first element wins)
+        disp[p] = static_cast<float>(d_min + bi);
+    }
+}
+
+// ----------------------------------------------------- histogram refine ----
+// refine_disparity_histogram, stereo.cpp:240-299. bin_max over the input.
+__global__ void k_bin_max(const float* __restrict__ disp, int n, int* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int b = 0;
+    if (i < n) {
+        float v = disp[i];
+        if (isfinite(v)) b = max(0, static_cast<int>(lroundf(v)));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, off));
+    if ((threadIdx.x & 31) == 0 && b > 0) atomicMax(out, b);
+}
+
+// One warp per pixel, one lane per region row (rows beyond 32 loop); a
+// per-warp shared-memory histogram of nbins counters; mode = max count with
+// the smaller bin winning ties, as the reference's ascending scan does.
+__global__ void k_hist_refine(const float* __restrict__ cur, int w, int h,
+                              const uint8_t* __restrict__ L, const uint8_t* __restrict__ R,
+                              const uint8_t* __restrict__ U, const uint8_t* __restrict__ D,
+                              const int* __restrict__ bin_max_ptr, int nbins_cap,
+                              float* __restrict__ next) {
+    extern __shared__ unsigned hist_all[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned* hist = hist_all + static_cast<size_t>(warp) * nbins_cap;
+    const int bin_max = *bin_max_ptr;
+    const int nb = min(bin_max + 1, nbins_cap);
+    for (int b = lane; b < nb; b += 32) hist[b] = 0u;
+    __syncwarp();
+    const size_t p = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (p >= static_cast<size_t>(w) * h) return;
+    const float center = cur[p];
+    if (!isfinite(center)) {
+        if (lane == 0) next[p] = center;  // removed outliers stay removed
+        return;
+    }
+    const int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
+    const int up = U[p], dn = D[p];
+    int count = 0, lo = bin_max, hi = 0;
+    for (int r = -up + lane; r <= dn; r += 32) {
+        int vy = y + r;
+        size_t vi = static_cast<size_t>(vy) * w + x;
+        const float* row = cur + static_cast<size_t>(vy) * w;
+        for (int c = -static_cast<int>(L[vi]); c <= static_cast<int>(R[vi]); ++c) {
+            float v = row[x + c];
+            if (!isfinite(v)) continue;
+            int bin = static_cast<int>(lroundf(v));
+            bin = min(max(bin, 0), nb - 1);
+            atomicAdd(&hist[bin], 1u);
+            ++count;
+            lo = min(lo, bin);
+            hi = max(hi, bin);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        count += __shfl_xor_sync(0xffffffffu, count, off);
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+    }
+    __syncwarp();
+    int best_c = 0, best_b = lo;
+    for (int b = lo + lane; b <= hi; b += 32) {
+        int cnt = static_cast<int>(hist[b]);
+        if (cnt > best_c) {  // ascending within the lane: first max kept
+            best_c = cnt;
+            best_b = b;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        int oc = __shfl_xor_sync(0xffffffffu, best_c, off);
+        int ob = __shfl_xor_sync(0xffffffffu, best_b, off);
+        if (oc > best_c || (oc == best_c && ob < best_b)) {
+            best_c = oc;
+            best_b = ob;
+        }
+    }
+    if (lane == 0) {
+        if (best_c == 1 && count >= 4)
+            next[p] = __int_as_float(0x7fc00000);  // quiet NaN nodata
+        else
+            next[p] = static_cast<float>(best_c > 0 ? best_b : lo);
+    }
+}
+
+// Clears the per-warp histograms is done at kernel start; nothing persists.
+
+// -------------------------------------------------------- sparse depth -----
+// disparity_to_sparse_depth, stereo.cpp:301-315.
+__global__ void k_sparse_depth(const float* __restrict__ disp, int w, int h, double fb, int fw,
+                               int fh, float* __restrict__ out) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= fw || y >= fh) return;
+    float v = __int_as_float(0x7fc00000);
+    if (!(x & 1) && !(y & 1) && (x >> 1) < w && (y >> 1) < h) {
+        float d = disp[static_cast<size_t>(y >> 1) * w + (x >> 1)];
+        if (isfinite(d)) {
+            double d_full = 2.0 * static_cast<double>(d);
+            if (d_full > 0.0) v = static_cast<float>(fb / d_full);
+        }
+    }
+    out[static_cast<size_t>(y) * fw + x] = v;
+}
+
+__global__ void k_max_arm(const uint8_t* __restrict__ a0, const uint8_t* __restrict__ a1,
+                          const uint8_t* __restrict__ a2, const uint8_t* __restrict__ a3, size_t n,
+                          int* __restrict__ out) {
+    size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int m = 0;
+    if (i < n) m = max(max(a0[i], a1[i]), max(a2[i], a3[i]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out, m);
+}
+
+inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
+
+int ring_size(int l1) {
+    int need = 2 * l1 + 2, r = 1;
+    while (r < need) r <<= 1;
+    return r;
+}
+
+}  // namespace
+
+// ===================================================================== host =
+
+int max_arm_length(dco_ctx* ctx, const uint8_t* l, const uint8_t* r, const uint8_t* u,
+                   const uint8_t* d, int w, int h) {
+    size_t n = static_cast<size_t>(w) * h;
+    int* dm = static_cast<int*>(scratch(ctx, S_FLAG_ARM, 64));
+    cuda_check(cudaMemsetAsync(dm, 0, sizeof(int), ctx->stream), "memset");
+    k_max_arm<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(l, r, u, d, n, dm);
+    launched(ctx, "k_max_arm");
+    int* hm = static_cast<int*>(pinned_host(ctx, 64));
+    cuda_check(cudaMemcpyAsync(hm, dm, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+    return *hm;
+}
+
+void downsample_half(dco_ctx* ctx, const float* img, int w, int h, float* out) {
+    require(w >= 2 && h >= 2, "downsample_half: dimensions must be at least 2x2");
+    int ow = w / 2, oh = h / 2;
+    dim3 b(32, 8);
+    k_downsample<<<grid2(ow, oh, b), b, 0, ctx->stream>>>(img, w, h, out, ow, oh);
+    launched(ctx, "k_downsample");
+}
+
+void ingest_gray8(dco_ctx* ctx, const uint8_t* g8, int w, int h, float* full, float* quarter) {
+    require(w >= 2 && h >= 2, "ingest: dimensions must be at least 2x2");
+    int qw = w / 2, qh = h / 2;
+    dim3 b(32, 8);
+    k_ingest_gray8<<<grid2(qw, qh, b), b, 0, ctx->stream>>>(g8, w, h, full, quarter, qw, qh);
+    launched(ctx, "k_ingest_gray8");
+    int tail = ((w & 1) ? h : 0) + ((h & 1) ? w : 0);
+    if (full && tail) {
+        k_ingest_gray8_tail<<<blocks_for(tail, 256), 256, 0, ctx->stream>>>(g8, w, h, full);
+        launched(ctx, "k_ingest_gray8_tail");
+    }
+}
+
+void build_cross_windows(dco_ctx* ctx, const float* img, int w, int h, const dco_config* cfg,
+                         uint8_t* l, uint8_t* r, uint8_t* u, uint8_t* d) {
+    require(w >= 1 && h >= 1, "build_cross_windows: empty image");
+    require(cfg->cross_arm_l1 <= 255, "build_cross_windows: cross_arm_l1 must fit the u8 arms");
+    uint8_t* raw = static_cast<uint8_t*>(scratch(ctx, S_ARM_RAW, static_cast<size_t>(w) * h * 4));
+    dim3 b(32, 8);
+    k_cross_arms_raw<<<grid2(w, h, b), b, 0, ctx->stream>>>(img, w, h, cfg->cross_arm_l1,
+                                                            cfg->cross_arm_l2, cfg->cross_color_tau,
+                                                            cfg->cross_color_tau2, raw);
+    launched(ctx, "k_cross_arms_raw");
+    dim3 g = grid2(w, h, b);
+    g.z = 4;
+    k_arm_median<<<g, b, 0, ctx->stream>>>(raw, w, h, l, r, u, d);
+    launched(ctx, "k_arm_median");
+}
+
+void census_transform(dco_ctx* ctx, const float* img, int w, int h, int ww, int wh, uint64_t* out) {
+    if (ww % 2 == 0 || wh % 2 == 0)
+        fail(DCO_CONFIG, "census_transform: window dimensions must be odd");
+    if (ww * wh - 1 > 64) fail(DCO_CONFIG, "census_transform: window exceeds 64 comparison bits");
+    dim3 b(32, 8);
+    k_census<<<grid2(w, h, b), b, 0, ctx->stream>>>(img, w, h, ww / 2, wh / 2, out);
+    launched(ctx, "k_census");
+}
+
+void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, int w, int h,
+                         const uint8_t* l, const uint8_t* r, const uint8_t* u, const uint8_t* d,
+                         const dco_config* cfg, float* cost) {
+    validate_config(cfg);
+    const size_t n = static_cast<size_t>(w) * h;
+    uint64_t* census = static_cast<uint64_t*>(scratch(ctx, S_CENSUS, n * 16));
+    census_transform(ctx, left, w, h, cfg->census_window_w, cfg->census_window_h, census);
+    census_transform(ctx, right, w, h, cfg->census_window_w, cfg->census_window_h, census + n);
+    CostParams hp;
+    hp.w = w;
+    hp.h = h;
+    hp.nd = cfg->d_max - cfg->d_min + 1;
+    hp.d_min = cfg->d_min;
+    hp.bits = cfg->census_window_w * cfg->census_window_h - 1;
+    hp.lambda_ad = cfg->lambda_ad;
+    StereoTables t;
+    make_stereo_tables(cfg, &t);
+    for (int i = 0; i < 256; ++i) hp.alpha[i] = t.alpha[i];
+    for (int i = 0; i < 65; ++i) hp.census[i] = t.census[i];
+    const size_t total = n * hp.nd;
+    int dev_sms = 148;
+    unsigned blocks = static_cast<unsigned>(std::min<size_t>(blocks_for(total, 256), dev_sms * 16));
+    k_cost_volume<<<blocks, 256, 0, ctx->stream>>>(left, right, census, census + n, l, r, u, d, hp,
+                                                   cost);
+    launched(ctx, "k_cost_volume");
+}
+
+void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l,
+                     const uint8_t* r, const uint8_t* u, const uint8_t* d, int max_arm,
+                     float* out) {
+    require(nd >= 1, "aggregate_costs: empty disparity range");
+    const size_t n = static_cast<size_t>(w) * h;
+    int* region = static_cast<int*>(scratch(ctx, S_REGION, n * sizeof(int)));
+    double* hsum = static_cast<double*>(scratch(ctx, S_HSUM, n * nd * sizeof(double)));
+    dim3 b(32, 8);
+    k_region_size<<<grid2(w, h, b), b, 0, ctx->stream>>>(l, r, u, d, w, h, region);
+    launched(ctx, "k_region_size");
+    require(max_arm >= 0 && max_arm <= 255, "aggregate_costs: arm length out of range");
+    const int lag = max_arm + 1, ring = ring_size(max_arm);
+    int rows = 4;
+    while (rows > 1 && static_cast<size_t>(ring) * 32 * rows * sizeof(double) > 200 * 1024) rows >>= 1;
+    dim3 tb(32, rows);
+    size_t smem = static_cast<size_t>(ring) * 32 * rows * sizeof(double);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_agg_hpass, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_agg_vpass, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_set = true;
+    }
+    dim3 gh((nd + 31) / 32, (h + rows - 1) / rows);
+    k_agg_hpass<<<gh, tb, smem, ctx->stream>>>(cost, w, h, nd, l, r, lag, ring - 1, hsum);
+    launched(ctx, "k_agg_hpass");
+    dim3 gv((nd + 31) / 32, (w + rows - 1) / rows);
+    k_agg_vpass<<<gv, tb, smem, ctx->stream>>>(hsum, w, h, nd, u, d, region, lag, ring - 1, out);
+    launched(ctx, "k_agg_vpass");
+}
+
+void select_disparity_wta(dco_ctx* ctx, const float* cost, int w, int h, int d_min, int nd,
+                          float* disp) {
+    const size_t n = static_cast<size_t>(w) * h;
+    k_wta<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(cost, static_cast<int>(n), nd, d_min,
+                                                            disp);
+    launched(ctx, "k_wta");
+}
+
+void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
+                                const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters,
+                                int bin_bound, float* out) {
+    const size_t n = static_cast<size_t>(w) * h;
+    require(iters >= 0, "refine_disparity_histogram: negative iteration count");
+    if (iters == 0) {
+        cuda_check(cudaMemcpyAsync(out, disp, n * 4, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+        return;
+    }
+    int* bmax = static_cast<int*>(scratch(ctx, S_FLAG_BIN, 64));
+    cuda_check(cudaMemsetAsync(bmax, 0, sizeof(int), ctx->stream), "memset");
+    k_bin_max<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(disp, static_cast<int>(n), bmax);
+    launched(ctx, "k_bin_max");
+    int cap = bin_bound + 1;
+    if (bin_bound < 0) {  // unknown input range: read the bound back
+        int hb = 0;
+        cuda_check(cudaMemcpyAsync(&hb, bmax, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        cap = hb + 1;
+    }
+    require(cap <= 8192, "refine_disparity_histogram: disparities above 8191 are not supported");
+    cap = (cap + 31) & ~31;
+    const int warps = 8;
+    size_t smem = static_cast<size_t>(warps) * cap * sizeof(unsigned);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_hist_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_set = true;
+    }
+    float* bufs[2] = {static_cast<float*>(scratch(ctx, S_DISP0, n * 4)),
+                      static_cast<float*>(scratch(ctx, S_DISP1, n * 4))};
+    const float* src = disp;
+    for (int it = 0; it < iters; ++it) {
+        float* dst = (it == iters - 1) ? out : bufs[it & 1];
+        k_hist_refine<<<blocks_for(n * 32, warps * 32), warps * 32, smem, ctx->stream>>>(
+            src, w, h, l, r, u, d, bmax, cap, dst);
+        launched(ctx, "k_hist_refine");
+        src = dst;
+    }
+}
+
+void disparity_to_sparse_depth(dco_ctx* ctx, const float* disp, int w, int h, const dco_config* cfg,
+                               int fw, int fh, float* out) {
+    if (fw < w * 2 || fh < h * 2)
+        fail(DCO_INPUT, "disparity_to_sparse_depth: full dimensions too small for the quarter map");
+    dim3 b(32, 8);
+    k_sparse_depth<<<grid2(fw, fh, b), b, 0, ctx->stream>>>(disp, w, h, cfg->focal_px * cfg->baseline_m,
+                                                            fw, fh, out);
+    launched(ctx, "k_sparse_depth");
+}
+
+}  // namespace dco_gpu
+
+using namespace dco_gpu;
+
+extern "C" {
+
+int dco_downsample_half(dco_ctx* ctx, const float* img, int w, int h, float* out) {
+    return guarded(ctx, [&] { downsample_half(ctx, img, w, h, out); });
+}
+
+int dco_ingest_gray8(dco_ctx* ctx, const uint8_t* g8, int w, int h, float* full, float* quarter) {
+    return guarded(ctx, [&] { ingest_gray8(ctx, g8, w, h, full, quarter); });
+}
+
+int dco_build_cross_windows(dco_ctx* ctx, const float* img, int w, int h, const dco_config* cfg,
+                            uint8_t* l, uint8_t* r, uint8_t* u, uint8_t* d) {
+    return guarded(ctx, [&] { build_cross_windows(ctx, img, w, h, cfg, l, r, u, d); });
+}
+
+int dco_census_transform(dco_ctx* ctx, const float* img, int w, int h, int ww, int wh, uint64_t* out) {
+    return guarded(ctx, [&] { census_transform(ctx, img, w, h, ww, wh, out); });
+}
+
+int dco_compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, int w, int h,
+                            const uint8_t* l, const uint8_t* r, const uint8_t* u, const uint8_t* d,
+                            const dco_config* cfg, float* cost) {
+    return guarded(ctx, [&] { compute_cost_volume(ctx, left, right, w, h, l, r, u, d, cfg, cost); });
+}
+
+int dco_aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int d_min, int d_max,
+                        const uint8_t* l, const uint8_t* r, const uint8_t* u, const uint8_t* d,
+                        float* out) {
+    return guarded(ctx, [&] {
+        require(d_max >= d_min, "aggregate_costs: empty disparity range");
+        // the ring must cover the longest arm present: reduce it on the device
+        aggregate_costs(ctx, cost, w, h, d_max - d_min + 1, l, r, u, d,
+                        max_arm_length(ctx, l, r, u, d, w, h), out);
+    });
+}
+
+int dco_select_disparity_wta(dco_ctx* ctx, const float* cost, int w, int h, int d_min, int d_max,
+                             float* disp) {
+    return guarded(ctx, [&] {
+        require(d_max >= d_min, "select_disparity_wta: empty disparity range");
+        select_disparity_wta(ctx, cost, w, h, d_min, d_max - d_min + 1, disp);
+    });
+}
+
+int dco_refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
+                                   const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters,
+                                   float* out) {
+    return guarded(ctx, [&] { refine_disparity_histogram(ctx, disp, w, h, l, r, u, d, iters, -1, out); });
+}
+
+int dco_disparity_to_sparse_depth(dco_ctx* ctx, const float* disp, int w, int h, const dco_config* cfg,
+                                  int fw, int fh, float* out) {
+    return guarded(ctx, [&] { disparity_to_sparse_depth(ctx, disp, w, h, cfg, fw, fh, out); });
+}
+
+}  // extern "C"

@@ -1,0 +1,180 @@
+"""Densify (assembly bit-exact, PCG+MR within tolerance), composite (exact)
+and the device-resident frame stream vs the reference (densify.cpp,
+occlude.cpp:171-194, pipeline.cpp:136-258).
+
+Tolerances: dense depth max-abs <= 1e-5 m and RMS <= 1e-6 m
+versus the oracle's sequential-order solve; iteration counts within +-2 of
+the oracle's; objective values within 1e-9 relative."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2203_02300_b200.config import Config, InputError, UnsolvableFrameError
+from tests.inputs import Rng, scene
+from tests.test_gpu_stereo import N, T, bits_equal
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 1e-5
+RMS = 1e-6
+
+
+def random_inputs(w, h, seed, with_pre):
+    rng = Rng(seed)
+    sparse = np.full((h, w), np.nan, np.float32)
+    edges = np.zeros((h, w), np.uint8)
+    m_i = np.zeros((h, w), np.float32)
+    pre = np.full((h, w), np.nan, np.float32)
+    for y in range(h):
+        for x in range(w):
+            if rng.uniform() < 0.25:
+                sparse[y, x] = rng.uniform(0.5, 4.0)
+            edges[y, x] = 1 if rng.uniform() < 0.08 else 0
+            m_i[y, x] = rng.uniform()
+            if rng.uniform() < 0.5:
+                pre[y, x] = rng.uniform(0.5, 4.0)
+    m_fuse = np.array([rng.uniform() for _ in range((w // 2) * (h // 2))], np.float32).reshape(h // 2, w // 2)
+    return sparse, edges, m_fuse, m_i, (pre if with_pre else None)
+
+
+def gpu_sys_arrays(sys):
+    return {k: N(getattr(sys, k)) for k in ("diag", "coup_h", "coup_v", "rhs", "initial", "anchored")}
+
+
+@pytest.mark.parametrize("seed,with_pre", [(5150, False), (5151, True), (9, True)])
+def test_assemble_bit_exact_random(gpu, ref, seed, with_pre):
+    cfg = Config()
+    sparse, edges, m_fuse, m_i, pre = random_inputs(16, 16, seed, with_pre)
+    want = ref.assemble_system(sparse, edges, m_fuse, m_i, pre, cfg)
+    sys = gpu.assemble_system(T(sparse), T(edges), T(m_fuse), T(m_i), None if pre is None else T(pre), cfg)
+    got = gpu_sys_arrays(sys)
+    for k in ("diag", "coup_h", "coup_v", "rhs", "initial", "anchored"):
+        assert bits_equal(got[k], want[k]), k
+    assert sys.anchor_count == want["anchor_count"]
+    assert abs(sys.constant_term - want["constant_term"]) <= 1e-12 * max(1.0, abs(want["constant_term"]))
+
+
+def test_smoothness_weight(gpu, ref):
+    sparse, edges, m_fuse, m_i, _ = random_inputs(12, 10, 3, False)
+    for (px, py, qx, qy) in [(0, 0, 1, 0), (3, 4, 3, 5), (11, 9, 10, 9), (5, 5, 5, 4)]:
+        assert gpu.smoothness_weight(px, py, qx, qy, T(edges), T(m_fuse), T(m_i)) == \
+            ref.smoothness_weight(px, py, qx, qy, edges, m_fuse, m_i)
+    with pytest.raises(InputError):
+        gpu.smoothness_weight(0, 0, 1, 1, T(edges), T(m_fuse), T(m_i))
+
+
+def _solve_both(gpu, ref, sparse, edges, m_fuse, m_i, pre, cfg):
+    want_sys = ref.assemble_system(sparse, edges, m_fuse, m_i, pre, cfg)
+    want, st = ref.solve_dense_depth(want_sys, cfg)
+    sys = gpu.assemble_system(T(sparse), T(edges), T(m_fuse), T(m_i), None if pre is None else T(pre), cfg)
+    got, gst = gpu.solve_dense_depth(sys, cfg)
+    return N(got), gst, want, st
+
+
+@pytest.mark.parametrize("seed,with_pre", [(5150, False), (5151, True), (77, False)])
+def test_solve_small_within_tolerance(gpu, ref, seed, with_pre):
+    cfg = Config(solver_tol=1e-12, solver_max_iter=3000)
+    got, gst, want, st = _solve_both(gpu, ref, *random_inputs(16, 16, seed, with_pre), cfg)
+    d = np.abs(got.astype(np.float64) - want)
+    assert d.max() <= MAX_ABS and np.sqrt((d ** 2).mean()) <= RMS
+    assert abs(gst.iterations - st["iterations"]) <= 2
+    assert gst.objective_final <= gst.objective_initial + 1e-9
+
+
+def test_solve_scene_within_tolerance(gpu, ref):
+    """A real frame's system (640x360 full res) with and without d_pre."""
+    cfg = Config(d_max=63)
+    fs = [scene(ref, 640, 360, index=i, seed=61) for i in range(4)]
+    q = [ref.downsample_half(f["left"]) for f in fs]
+    out = ref.pipeline_frame(q[0], q[1], q[2], fs[1]["left"], ref.downsample_half(fs[1]["right"]),
+                             np.repeat(fs[1]["left"][:, :, None], 3, 2), None, None, None, cfg)
+    # rebuild the pipeline's system inputs with the oracle
+    fp, ff = ref.compute_flow(q[1], q[0], cfg), ref.compute_flow(q[1], q[2], cfg)
+    mp = ref.gradient_amplitude(ref.flow_to_polar(*fp)[0])
+    mf = ref.gradient_amplitude(ref.flow_to_polar(*ff)[0])
+    m_fuse = ref.normalize_amplitude(ref.box_filter(ref.fuse_amplitudes(fp, ff, mp, mf, cfg), cfg.box_radius))
+    edges, m_i = ref.extract_depth_contours_prefiltered(ref.gaussian_blur(fs[1]["left"], cfg.gauss_sigma), m_fuse, cfg)
+    assert bits_equal(edges, out["edges"])
+    for pre in (None, out["dense"]):
+        got, gst, want, st = _solve_both(gpu, ref, out["sparse"], edges, m_fuse, m_i, pre, cfg)
+        d = np.abs(got.astype(np.float64) - want)
+        assert d.max() <= MAX_ABS, d.max()
+        assert np.sqrt((d ** 2).mean()) <= RMS
+        assert abs(gst.iterations - st["iterations"]) <= 2, (gst.iterations, st["iterations"])
+        assert abs(gst.objective_final - st["objective_final"]) <= 1e-9 * abs(st["objective_final"]) + 1e-9
+
+
+def test_unsolvable(gpu, ref):
+    cfg = Config()
+    h, w = 8, 8
+    sparse = np.full((h, w), np.nan, np.float32)
+    edges = np.zeros((h, w), np.uint8)
+    m_i = np.zeros((h, w), np.float32)
+    m_fuse = np.zeros((4, 4), np.float32)
+    sys = gpu.assemble_system(T(sparse), T(edges), T(m_fuse), T(m_i), None, cfg)
+    assert sys.anchor_count == 0
+    with pytest.raises(UnsolvableFrameError):
+        gpu.solve_dense_depth(sys, cfg)
+
+
+def test_apply_and_objective(gpu, ref):
+    cfg = Config()
+    sparse, edges, m_fuse, m_i, pre = random_inputs(16, 12, 4, True)
+    want = ref.assemble_system(sparse, edges, m_fuse, m_i, pre, cfg)
+    sys = gpu.assemble_system(T(sparse), T(edges), T(m_fuse), T(m_i), T(pre), cfg)
+    x = np.random.default_rng(1).random((12, 16))
+    assert bits_equal(N(gpu.apply_system(sys, T(x))), ref.apply_system(want, x))
+    obj = gpu.objective_value(sys, T(x))
+    assert np.isfinite(obj)
+
+
+def test_composite_exact(gpu, ref):
+    # criterion_composite_exhaustive (acceptance.cpp:637-669)
+    rng = np.random.default_rng(64646)
+    h, w = 64, 64
+    real = rng.random((h, w, 3), dtype=np.float32)
+    dense = np.where(rng.random((h, w)) < 0.9, rng.uniform(0.2, 3.0, (h, w)), np.nan).astype(np.float32)
+    vrgb = rng.random((h, w, 3), dtype=np.float32)
+    vdepth = np.where(rng.random((h, w)) < 0.7, rng.uniform(0.2, 3.0, (h, w)), np.nan).astype(np.float32)
+    vdepth[0, :8] = dense[0, :8]  # ties go to the virtual layer
+    want_c, want_m = ref.composite(real, dense, vrgb, vdepth)
+    got_c, got_m = gpu.composite(T(real), T(dense), T(vrgb), T(vdepth))
+    assert bits_equal(N(got_c), want_c) and bits_equal(N(got_m), want_m)
+
+
+def test_stream_matches_reference_pipeline(gpu, ref):
+    """Five frames through dco_stream (device-resident window, d_pre chain,
+    composite against a rendered cube) vs ref_pipeline_frame per window."""
+    W, H = 320, 192
+    cfg = Config(d_max=47)
+    fs = [scene(ref, W, H, index=i, seed=1234) for i in range(5)]
+    vrgb, vdepth = ref.render_cube(W, H, cfg.focal_px, cz=1.5, side=0.3)
+    s = gpu.Stream(W, H, cfg)
+    s.set_virtual(T(vrgb), T(vdepth))
+    prev = None
+    for i, f in enumerate(fs):
+        res = s.push_gray8(T(f["left8"]), T(f["right8"]))
+        if i < 2:
+            assert res.composited == 0
+            continue
+        assert res.composited == 1
+        q = [ref.downsample_half(fs[j]["left"]) for j in (i - 2, i - 1, i)]
+        mid = fs[i - 1]
+        want = ref.pipeline_frame(q[0], q[1], q[2], mid["left"], ref.downsample_half(mid["right"]),
+                                  np.repeat(mid["left"][:, :, None], 3, 2), prev, vrgb, vdepth, cfg)
+        v = s.views()
+        dense = N(gpu.view_tensor(v.dense, (H, W), torch.float32))
+        edges = N(gpu.view_tensor(v.edges, (H, W), torch.uint8))
+        sparse = N(gpu.view_tensor(v.sparse, (H, W), torch.float32))
+        mask = N(gpu.view_tensor(v.mask, (H, W), torch.uint8))
+        assert bits_equal(sparse, want["sparse"])
+        assert bits_equal(edges, want["edges"])
+        d = np.abs(dense.astype(np.float64) - want["dense"])
+        assert d.max() <= MAX_ABS and np.sqrt((d ** 2).mean()) <= RMS
+        assert abs(res.densify_iterations - want["iterations"]) <= 2
+        # the mask is a depth test against the dense map: equal wherever the
+        # virtual depth is not within the solver tolerance of the real depth
+        close = np.abs(vdepth - want["dense"]) <= 2 * MAX_ABS
+        assert ((mask == want["mask"]) | close).all()
+        prev = want["dense"]
+    s.close()

@@ -1,0 +1,158 @@
+"""Flow and depth-contour stages on the GPU vs the reference, bit for bit
+(flow.cpp, contour.cpp)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2203_02300_b200.config import Config, InputError
+from tests.inputs import Rng, random_image, scene
+from tests.test_gpu_stereo import N, T, bits_equal, mismatch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=[(320, 192, 1234), (640, 360, 61)], ids=lambda p: "%dx%d" % p[:2])
+def frames(request, ref):
+    w, h, seed = request.param
+    fs = [scene(ref, w, h, index=i, seed=seed) for i in range(3)]
+    q = [ref.downsample_half(f["left"]) for f in fs]
+    return dict(fs=fs, q=q, w=w, h=h)
+
+
+def test_flow_bit_exact(gpu, ref, frames):
+    cfg = Config()
+    past, mid, fut = frames["q"]
+    for to in (past, fut):
+        u, v = gpu.compute_flow(T(mid), T(to), cfg)
+        ur, vr = ref.compute_flow(mid, to, cfg)
+        assert mismatch(N(u), ur) == 0
+        assert mismatch(N(v), vr) == 0
+
+
+def test_flow_translation_kat(gpu, ref):
+    # criterion_flow (acceptance.cpp:265-322) on a smooth texture: GPU == oracle
+    rng = Rng(11)
+    h, w = 96, 128
+    p1, p2, p3 = rng.uniform(0, 6.28), rng.uniform(0, 6.28), rng.uniform(0, 6.28)
+    tau = 6.283185307179586
+    yy, xx = np.mgrid[0:h, 0:w]
+    u, v = xx / w, yy / h
+    val = (0.5 + 0.17 * np.sin(tau * 3 * u + p1) * np.cos(tau * 2 * v + p2) + 0.15 * np.sin(tau * 5 * v + p3)
+           + 0.11 * np.sin(tau * (4 * u + 3 * v) + p1) + 0.07 * np.sin(tau * 8 * u + p2) * np.sin(tau * 6 * v + p3))
+    base = np.clip(val, 0, 1).astype(np.float32)
+    cfg = Config()
+    for sx, sy in [(4, 0), (-4, 0), (0, 3), (-3, 2)]:
+        moved = np.roll(np.roll(base, -sy, axis=0), -sx, axis=1)
+        gu, gv = gpu.compute_flow(T(moved), T(base), cfg)
+        ru, rv = ref.compute_flow(moved, base, cfg)
+        assert bits_equal(N(gu), ru) and bits_equal(N(gv), rv)
+        assert abs(np.median(N(gu)) - sx) <= 0.5 and abs(np.median(N(gv)) - sy) <= 0.5
+
+
+def test_flow_rejects_small_frames(gpu):
+    with pytest.raises(InputError):
+        gpu.compute_flow(T(random_image(7, 20, 1)), T(random_image(7, 20, 2)), Config())
+
+
+def test_polar_amplitude_fusion_box_normalize(gpu, ref, frames):
+    cfg = Config()
+    past, mid, fut = frames["q"]
+    fp = ref.compute_flow(mid, past, cfg)
+    ff = ref.compute_flow(mid, fut, cfg)
+    rp, tp = ref.flow_to_polar(*fp)
+    r_g, t_g = gpu.flow_to_polar(T(fp[0]), T(fp[1]))
+    assert bits_equal(N(r_g), rp) and bits_equal(N(t_g), tp)
+    mp = ref.gradient_amplitude(rp)
+    assert bits_equal(N(gpu.gradient_amplitude(T(rp))), mp)
+    mf = ref.gradient_amplitude(ref.flow_to_polar(*ff)[0])
+    fused = ref.fuse_amplitudes(fp, ff, mp, mf, cfg)
+    got = gpu.fuse_amplitudes((T(fp[0]), T(fp[1])), (T(ff[0]), T(ff[1])), T(mp), T(mf), cfg)
+    assert bits_equal(N(got), fused)
+    boxed = ref.box_filter(fused, cfg.box_radius)
+    assert bits_equal(N(gpu.box_filter(T(fused), cfg.box_radius)), boxed)
+    assert bits_equal(N(gpu.normalize_amplitude(T(boxed))), ref.normalize_amplitude(boxed))
+
+
+def test_fusion_random_oracle(gpu, ref):
+    # criterion_fusion_oracle (acceptance.cpp:328-381): random flows with zeros
+    rng = Rng(31415)
+    cfg = Config()
+    for trial in range(20):
+        w, h = rng.uniform_int(5, 16), rng.uniform_int(5, 14)
+        a = np.array([rng.uniform(-3, 3) for _ in range(4 * w * h)], np.float32).reshape(4, h, w)
+        a[0:2, :, ::3] = 0.0
+        mp, mf = random_image(w, h, trial), random_image(w, h, trial + 100)
+        want = ref.fuse_amplitudes((a[0], a[1]), (a[2], a[3]), mp, mf, cfg)
+        got = gpu.fuse_amplitudes((T(a[0]), T(a[1])), (T(a[2]), T(a[3])), T(mp), T(mf), cfg)
+        assert bits_equal(N(got), want)
+
+
+def test_box_filter_radii_and_nan(gpu, ref):
+    a = random_image(53, 29, 9)
+    for r in (1, 3, 5, 40):
+        assert bits_equal(N(gpu.box_filter(T(a), r)), ref.box_filter(a, r))
+    with pytest.raises(InputError):
+        gpu.box_filter(T(a), 0)
+    b = a.copy()
+    b[3, 4] = np.nan
+    assert bits_equal(N(gpu.normalize_amplitude(T(b))), ref.normalize_amplitude(b))
+    z = np.zeros((9, 9), np.float32)
+    assert bits_equal(N(gpu.normalize_amplitude(T(z))), ref.normalize_amplitude(z))
+
+
+def test_gaussian_and_contours_bit_exact(gpu, ref, frames):
+    cfg = Config()
+    past, mid, fut = frames["q"]
+    fp, ff = ref.compute_flow(mid, past, cfg), ref.compute_flow(mid, fut, cfg)
+    mp = ref.gradient_amplitude(ref.flow_to_polar(*fp)[0])
+    mf = ref.gradient_amplitude(ref.flow_to_polar(*ff)[0])
+    m_fuse = ref.normalize_amplitude(ref.box_filter(ref.fuse_amplitudes(fp, ff, mp, mf, cfg), cfg.box_radius))
+    gray = frames["fs"][1]["left"]
+    blurred = ref.gaussian_blur(gray, cfg.gauss_sigma)
+    assert bits_equal(N(gpu.gaussian_blur(T(gray), cfg.gauss_sigma)), blurred)
+    edges, m_i = ref.extract_depth_contours_prefiltered(blurred, m_fuse, cfg)
+    ge, gm = gpu.extract_depth_contours_prefiltered(T(blurred), T(m_fuse), cfg)
+    assert bits_equal(N(gm), m_i)
+    assert bits_equal(N(ge), edges)
+    assert edges.sum() > 0
+    ge2, gm2 = gpu.extract_depth_contours(T(gray), T(m_fuse), cfg)
+    assert bits_equal(N(ge2), edges) and bits_equal(N(gm2), m_i)
+
+
+def test_contours_ungated_and_thresholds(gpu, ref):
+    f = scene(ref, 320, 192, seed=1234)
+    gray = f["left"]
+    blurred = ref.gaussian_blur(gray, 1.4)
+    open_gate = np.ones((96, 160), np.float32)
+    for cfg in (Config(), Config(t_low=0.01, t_high=0.2), Config(t_depth=0.5)):
+        e, m = ref.extract_depth_contours_prefiltered(blurred, open_gate, cfg)
+        ge, gm = gpu.extract_depth_contours_prefiltered(T(blurred), T(open_gate), cfg)
+        assert bits_equal(N(ge), e) and bits_equal(N(gm), m)
+
+
+def test_contour_scene_kat(gpu, ref):
+    """criterion_contour_scene (acceptance.cpp:386-463) through the GPU stages:
+    recall 1.000000, suppression 0.982492, texture_edges 10738."""
+    kw = dict(square_size=80, square_x0=96.0, square_y0=56.0, shift_x=4.0, seed=1234)
+    fs = [ref.render_synth_frame(320, 192, i, **kw) for i in range(3)]
+    cfg = Config()
+    q = [gpu.downsample_half(T(f["left"])) for f in fs]
+    fp, ff = gpu.compute_flow(q[1], q[0], cfg), gpu.compute_flow(q[1], q[2], cfg)
+    mp = gpu.gradient_amplitude(gpu.flow_to_polar(*fp)[0])
+    mf = gpu.gradient_amplitude(gpu.flow_to_polar(*ff)[0])
+    fused = gpu.normalize_amplitude(gpu.box_filter(gpu.fuse_amplitudes(fp, ff, mp, mf, cfg), cfg.box_radius))
+    gated, _ = gpu.extract_depth_contours(T(fs[1]["left"]), fused, cfg)
+    ungated, _ = gpu.extract_depth_contours(T(fs[1]["left"]), torch.ones_like(fused), cfg)
+    gated, ungated, gt = N(gated), N(ungated), fs[1]["gt_boundary"]
+    h, w = gt.shape
+    from scipy.ndimage import maximum_filter
+
+    near2 = maximum_filter(gated, size=5, mode="constant")
+    recall = near2[gt == 1].astype(bool).mean()
+    reach = 2 * (cfg.box_radius + 5)
+    near_b = maximum_filter(gt, size=2 * reach + 1, mode="constant").astype(bool)
+    tex = ungated.astype(bool) & ~near_b
+    suppression = (~gated.astype(bool) & tex).sum() / tex.sum()
+    assert "%.6f" % recall == "1.000000"
+    assert "%.6f" % suppression == "0.982492"
+    assert int(tex.sum()) == 10738
