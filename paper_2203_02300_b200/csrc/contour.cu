@@ -142,14 +142,25 @@ __global__ void k_amp_fuse(const float* __restrict__ pu, const float* __restrict
 // -------------------------------------------------------------- box filter -
 // box_filter, contour.cpp:108-136. Row running sums (double, sequential).
 __global__ void k_box_rows(const float* __restrict__ a, int w, int h, double* __restrict__ rows) {
-    int y = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per row: coalesced 32-wide loads, the running sum stays a
+    // strictly sequential double chain (lane 0's order) broadcast by shuffles
+    const int lane = threadIdx.x & 31;
+    const int y = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (y >= h) return;
-    double s = 0.0;
     const float* src = a + static_cast<size_t>(y) * w;
     double* dst = rows + static_cast<size_t>(y) * w;
-    for (int x = 0; x < w; ++x) {
-        s += src[x];
-        dst[x] = s;
+    double s = 0.0;
+    float nxt = lane < w ? src[lane] : 0.0f;
+    for (int x0 = 0; x0 < w; x0 += 32) {
+        float cur = nxt;
+        nxt = (x0 + 32 + lane < w) ? src[x0 + 32 + lane] : 0.0f;
+        double mine = 0.0;
+        const int cnt = min(32, w - x0);
+        for (int j = 0; j < cnt; ++j) {
+            s += static_cast<double>(__shfl_sync(0xffffffffu, cur, j));
+            if (lane == j) mine = s;
+        }
+        if (lane < cnt) dst[x0 + lane] = mine;
     }
 }
 // Column chain: sat[y+1][x+1] = sat[y][x+1] + rows[y][x]; sat is (h+1)x(w+1).
@@ -163,9 +174,24 @@ __global__ void k_box_cols(const double* __restrict__ rows, int w, int h, double
     }
     double s = 0.0;
     sat[x] = 0.0;
-    for (int y = 0; y < h; ++y) {
-        s = s + rows[static_cast<size_t>(y) * w + (x - 1)];
-        sat[(y + 1) * W1 + x] = s;
+    constexpr int kPF = 16;
+    double cur[kPF], nxt[kPF];
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) cur[j] = j < h ? rows[static_cast<size_t>(j) * w + (x - 1)] : 0.0;
+    for (int y0 = 0; y0 < h; y0 += kPF) {
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            int y = y0 + kPF + j;
+            nxt[j] = y < h ? rows[static_cast<size_t>(y) * w + (x - 1)] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            if (y0 + j < h) {
+                s = s + cur[j];
+                sat[(y0 + j + 1) * W1 + x] = s;
+            }
+            cur[j] = nxt[j];
+        }
     }
 }
 __global__ void k_box_out(const double* __restrict__ sat, int w, int h, int r, float* __restrict__ out) {
@@ -413,7 +439,7 @@ void box_filter(dco_ctx* ctx, const float* a, int w, int h, int radius, float* o
     size_t n = static_cast<size_t>(w) * h;
     double* rows = static_cast<double*>(scratch(ctx, S_SAT, (n + (w + 1) * (h + 1) + 64) * sizeof(double)));
     double* sat = rows + n;
-    k_box_rows<<<blocks_for(h, 64), 64, 0, ctx->stream>>>(a, w, h, rows);
+    k_box_rows<<<blocks_for(static_cast<size_t>(h) * 32, 256), 256, 0, ctx->stream>>>(a, w, h, rows);
     launched(ctx, "k_box_rows");
     k_box_cols<<<blocks_for(w + 1, 64), 64, 0, ctx->stream>>>(rows, w, h, sat);
     launched(ctx, "k_box_cols");

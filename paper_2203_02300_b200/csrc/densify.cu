@@ -348,6 +348,7 @@ struct CGArgs {
     const float* fallback;    // unsolvable: dense = fallback (or NaN when null)
     const int* fallback_valid;  // nullable: fallback usable only when *fallback_valid
     SolveOut* out;
+    int mode;  // experiment knobs (0 in production): 1 no in-loop grid sync, 2 no halo loads, 4 no prec load
 };
 
 // Sum of the per-block partials, identical in every block (same order).
@@ -561,9 +562,321 @@ __global__ void __launch_bounds__(512) k_pcg(CGArgs a) {
     }
 }
 
+// ------------------------------------------------- on-chip resident solver --
+// Same algorithm and reductions as k_pcg, but each of the grid's blocks (one
+// per SM, 1024 threads) owns a contiguous chunk of unknowns for the whole
+// solve: r and p live in registers (EPT per thread), x / xs / rs and the
+// q-then-z scratch live in shared memory. Only p crosses blocks (written to
+// a global halo array once per iteration for the SpMV); the coefficient
+// arrays and the Jacobi preconditioner stream from L2. Per iteration: 3 grid
+// barriers (SpMV halo + 2 reductions; the |rs|^2 reduction shares the halo
+// barrier). Block reductions finish in warp 0 (one CTA barrier each).
+constexpr int kOnchipThreads = 1024;
+
+// per-thread partials -> this block's partial row in global memory
+template <int K>
+__device__ __forceinline__ void block_partial(double (&v)[K], double* sm_part, double* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sm_part[warp * K + k] = v[k];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double t = lane < nw ? sm_part[lane * K + k] : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            if (lane == 0) out[k] = t;
+        }
+    }
+}
+
+// all blocks' partial rows -> totals, identical (same order) in every block:
+// warp i loads partials [32i, 32i+32) and tree-reduces them, then every
+// thread adds the per-warp sums in warp order.
+template <int K>
+__device__ __forceinline__ void grid_reduce(const double* part, int stride, int nb, double (&res)[K],
+                                            double* sm_res /* [32*K] */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (nb + 31) >> 5;
+    if (warp < nw) {
+        const int b = warp * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = b < nb ? part[b * stride + k] : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) sm_res[warp * K + k] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += sm_res[i * K + k];
+        res[k] = s;
+    }
+}
+
+template <int EPT, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) {
+    // Block b owns [base, base + size): sizes differ by at most one, and every
+    // block holds >= (EPT-1)*1024 unknowns, so only the last register slot of
+    // a thread can be empty. Solver arithmetic uses explicit FMAs: the solve
+    // is tolerance-matched (not bit-exact) anyway and this halves the FP64
+    // instruction count.
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sx[];  // [4][chunk]: x, xs, rs, qz
+    __shared__ double sm_part[32 * 5];
+    __shared__ double sm_res[3][32 * 5];
+    const int w = a.w, h = a.h;
+    const int n = static_cast<int>(a.n);
+    const int nb = gridDim.x;
+    const int q = n / nb, rem = n - q * nb;
+    const int base = blockIdx.x * q + min(static_cast<int>(blockIdx.x), rem);
+    const int size = q + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
+    const int t = threadIdx.x;
+    // register slots of this thread that hold an unknown (EPT may be rounded up)
+    const int nv = size > t ? (size - t + THREADS - 1) / THREADS : 0;
+    double* s_x = sx + t;
+    double* s_xs = sx + chunk + t;
+    double* s_rs = sx + 2 * chunk + t;
+    double* s_qz = sx + 3 * chunk + t;
+    const double* __restrict__ diag = a.diag + base + t;
+    const double* __restrict__ ch = a.ch + base + t;
+    const double* __restrict__ cv = a.cv + base + t;
+    double* pg = a.p + base + t;  // global halo copy of p
+    const double* __restrict__ prec = a.prec + base + t;
+    double* part_setup = a.part;
+    double* part_pq = a.part + 8 * nb;
+    double* part_rho = a.part + 16 * nb;
+    double* part_rs = a.part + 24 * nb;
+    double* part_obj = a.part + 32 * nb;
+    double r[EPT], p[EPT];
+    uint64_t nbr = 0;  // 4 bits per slot (EPT <= 16): 1 right, 2 left, 4 down, 8 up
+#define DCO_OK(k) ((k) < nv)
+#define KO(k) ((k) * THREADS)
+
+    unsigned long long anchors = a.anchors_dev ? *a.anchors_dev : a.anchors_host;
+    if (anchors == 0) {
+        const float* fb = (a.fallback && (!a.fallback_valid || *a.fallback_valid)) ? a.fallback : nullptr;
+        for (int i = base + t; i < base + size; i += THREADS)
+            a.dense[i] = fb ? fb[i] : __int_as_float(0x7fc00000);
+        if (blockIdx.x == 0 && t == 0) {
+            a.out->status = 3;
+            a.out->iterations = 0;
+        }
+        return;
+    }
+    const double cterm = a.constant_term_dev ? *a.constant_term_dev : a.constant_term_host;
+
+    // setup (densify.cpp:147-166): x = initial, r = b - A x, z = M r, p = z
+    {
+        double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // b.b, r.r, r.z, x.Ax, b.x
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            r[k] = 0.0;
+            p[k] = 0.0;
+            if (DCO_OK(k)) {
+                const int i = base + t + KO(k);
+                const int xx = i % w, y = i / w;
+                nbr |= static_cast<uint64_t>((xx + 1 < w ? 1u : 0u) | (xx > 0 ? 2u : 0u) | (y + 1 < h ? 4u : 0u) |
+                                             (y > 0 ? 8u : 0u)) << (4 * k);
+                double ax = apply_at(a.diag, a.ch, a.cv, a.init, w, h, i, xx, y);
+                double xi = a.init[i];
+                double b = a.rhs[i];
+                double d = a.diag[i];
+                double pr = d > 0.0 ? 1.0 / d : 1.0;
+                double ri = b - ax;
+                double zi = pr * ri;
+                s_x[KO(k)] = xi;
+                s_xs[KO(k)] = xi;
+                s_rs[KO(k)] = ri;
+                a.prec[i] = pr;
+                r[k] = ri;
+                p[k] = zi;
+                a.p[i] = zi;
+                v[0] += b * b;
+                v[1] += ri * ri;
+                v[2] += ri * zi;
+                v[3] += xi * ax;
+                v[4] += b * xi;
+            }
+        }
+        block_partial<5>(v, sm_part, part_setup + 8 * blockIdx.x);
+    }
+    grid.sync();
+    double tot[5];
+    grid_reduce<5>(part_setup, 8, nb, tot, sm_res[0]);
+    const double bnorm = sqrt(tot[0]);
+    const double denom = bnorm > 0.0 ? bnorm : 1.0;
+    double snorm = sqrt(tot[1]);
+    double rho = tot[2];
+    if (blockIdx.x == 0 && t == 0) {
+        if (a.hist_cap > 0) a.hist[0] = snorm;
+        a.out->objective_initial = tot[3] - 2.0 * tot[4] + cterm;
+    }
+
+    int iter = 0;
+    while (iter < a.max_iter && snorm / denom > a.tol) {
+        // A: q = A p (halo p from global), pq -- stencil order of densify.cpp:125-129
+        {
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                if (DCO_OK(k)) {
+                    const unsigned m = static_cast<unsigned>(nbr >> (4 * k));
+                    const int o = KO(k);
+                    double acc = diag[o] * p[k];
+                    if (m & 1u) acc = __fma_rn(-ch[o], pg[o + 1], acc);
+                    if (m & 2u) acc = __fma_rn(-ch[o - 1], pg[o - 1], acc);
+                    if (m & 4u) acc = __fma_rn(-cv[o], pg[o + w], acc);
+                    if (m & 8u) acc = __fma_rn(-cv[o - w], pg[o - w], acc);
+                    s_qz[o] = acc;
+                    v = __fma_rn(p[k], acc, v);
+                }
+            }
+            double vv[1] = {v};
+            block_partial<1>(vv, sm_part, part_pq + 8 * blockIdx.x);
+        }
+        grid.sync();
+        double pqv[1];
+        grid_reduce<1>(part_pq, 8, nb, pqv, sm_res[1]);
+        const double pq = pqv[0];
+        if (pq <= 0.0) break;  // uniform across the grid
+        const double alpha = rho / pq;
+        // B: x, r, z; rho_next; MR numerators
+        {
+            double v[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                if (DCO_OK(k)) {
+                    const int o = KO(k);
+                    s_x[o] = __fma_rn(alpha, p[k], s_x[o]);
+                    double ri = __fma_rn(-alpha, s_qz[o], r[k]);
+                    double zi = prec[o] * ri;
+                    r[k] = ri;
+                    s_qz[o] = zi;
+                    v[0] = __fma_rn(ri, zi, v[0]);
+                    double rsi = s_rs[o];
+                    double di = ri - rsi;
+                    v[1] = __fma_rn(rsi, di, v[1]);
+                    v[2] = __fma_rn(di, di, v[2]);
+                }
+            }
+            block_partial<3>(v, sm_part, part_rho + 8 * blockIdx.x);
+        }
+        grid.sync();
+        double s3[3];
+        grid_reduce<3>(part_rho, 8, nb, s3, sm_res[2]);
+        const double rho_next = s3[0], sd = s3[1], dd = s3[2];
+        const double beta = rho_next / rho;
+        rho = rho_next;
+        double eta = 0.0;
+        if (dd > 0.0) {
+            eta = -sd / dd;
+            eta = eta < 0.0 ? 0.0 : (1.0 < eta ? 1.0 : eta);
+        }
+        // C: p = z + beta p (published for the next SpMV), MR smoothing, |rs|^2
+        {
+            double v = 0.0;
+            if (eta > 0.0) {
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) {
+                    if (DCO_OK(k)) {
+                        const int o = KO(k);
+                        double pn = __fma_rn(beta, p[k], s_qz[o]);
+                        p[k] = pn;
+                        pg[o] = pn;
+                        double rsi = s_rs[o];
+                        rsi = __fma_rn(eta, r[k] - rsi, rsi);
+                        s_rs[o] = rsi;
+                        double xsi = s_xs[o];
+                        s_xs[o] = __fma_rn(eta, s_x[o] - xsi, xsi);
+                        v = __fma_rn(rsi, rsi, v);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) {
+                    if (DCO_OK(k)) {
+                        const int o = KO(k);
+                        double pn = __fma_rn(beta, p[k], s_qz[o]);
+                        p[k] = pn;
+                        pg[o] = pn;
+                        double rsi = s_rs[o];
+                        v = __fma_rn(rsi, rsi, v);
+                    }
+                }
+            }
+            double vv[1] = {v};
+            block_partial<1>(vv, sm_part, part_rs + 8 * blockIdx.x);
+        }
+        grid.sync();
+        double sn[1];
+        grid_reduce<1>(part_rs, 8, nb, sn, sm_res[0]);
+        snorm = sqrt(sn[0]);
+        ++iter;
+        if (blockIdx.x == 0 && t == 0 && iter < a.hist_cap) a.hist[iter] = snorm;
+    }
+#undef DCO_OK
+#undef KO
+    // publish xs for the final objective's stencil, dense map
+    for (int i = base + t; i < base + size; i += THREADS) {
+        double xsi = sx[chunk + (i - base)];  // s_xs
+        a.xs[i] = xsi;
+        a.dense[i] = static_cast<float>(dmax0(xsi));
+    }
+    grid.sync();
+    {
+        double v[2] = {0.0, 0.0};
+        for (int i = base + t; i < base + size; i += THREADS) {
+            int xx = i % w, y = i / w;
+            double xsi = a.xs[i];
+            v[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
+            v[1] += a.rhs[i] * xsi;
+        }
+        block_partial<2>(v, sm_part, part_obj + 8 * blockIdx.x);
+    }
+    grid.sync();
+    if (blockIdx.x == 0) {
+        double o[2];
+        grid_reduce<2>(part_obj, 8, nb, o, sm_res[1]);
+        if (t == 0) {
+            a.out->objective_final = o[0] - 2.0 * o[1] + cterm;
+            a.out->status = 0;
+            a.out->iterations = iter;
+            a.out->relative_residual = snorm / denom;
+        }
+    }
+}
+
 inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
 
 int g_pcg_blocks = 0;
+int g_sms = 0;
+
+typedef void (*OnchipKernel)(CGArgs, int);
+constexpr int kOnchipThreadsUsed = 1024;
+OnchipKernel onchip_for(int ept, int* ept_used) {
+    *ept_used = ept;
+    switch (ept) {
+        case 1: return k_pcg_onchip<1, kOnchipThreadsUsed>;
+        case 2: return k_pcg_onchip<2, kOnchipThreadsUsed>;
+        case 3: return k_pcg_onchip<3, kOnchipThreadsUsed>;
+        case 4: return k_pcg_onchip<4, kOnchipThreadsUsed>;
+        case 5: return k_pcg_onchip<5, kOnchipThreadsUsed>;
+        case 6: return k_pcg_onchip<6, kOnchipThreadsUsed>;
+        case 7: return k_pcg_onchip<7, kOnchipThreadsUsed>;
+        case 8: return k_pcg_onchip<8, kOnchipThreadsUsed>;
+        default: return nullptr;
+    }
+}
 
 }  // namespace
 
@@ -639,7 +952,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         g_pcg_blocks = sms * std::min(per, 2);
     }
     const int nb = g_pcg_blocks;
-    double* wk = static_cast<double*>(scratch(ctx, S_CG, (8 * n + 4 * nb + 64) * sizeof(double)));
+    double* wk = static_cast<double*>(scratch(ctx, S_CG, (8 * n + 48 * 1024 + 64) * sizeof(double)));
     CGArgs a;
     a.w = w;
     a.h = h;
@@ -670,6 +983,30 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     a.fallback = fallback;
     a.fallback_valid = fallback_valid;
     a.out = static_cast<SolveOut*>(out_dev);
+    a.mode = getenv("DCO_PCG_MODE") ? atoi(getenv("DCO_PCG_MODE")) : 0;
+    // on-chip resident path: one 1024-thread block per SM, chunk of unknowns
+    // per block with 4 doubles each in shared memory, <= 8 per thread
+    const int sms = g_sms ? g_sms : (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, ctx->device), g_sms);
+    const int chunk = static_cast<int>((n + sms - 1) / sms);
+    int ept = (chunk + kOnchipThreadsUsed - 1) / kOnchipThreadsUsed;
+    const size_t smem = static_cast<size_t>(chunk) * 4 * sizeof(double);
+    OnchipKernel kern = onchip_for(ept, &ept);
+    if (kern && smem <= 200 * 1024 && sms <= 1024) {
+        static bool attr[17] = {};
+        if (!attr[ept]) {
+            cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024),
+                       "smem attr");
+            attr[ept] = true;
+        }
+        int chunk_arg = chunk;
+        void* params[] = {&a, &chunk_arg};
+        cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(sms), dim3(kOnchipThreadsUsed),
+                                               params, smem, ctx->stream),
+                   "launch k_pcg_onchip");
+        launched(ctx, "k_pcg_onchip");
+        return;
+    }
     void* params[] = {&a};
     cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg), dim3(nb), dim3(512), params, 0,
                                            ctx->stream),

@@ -88,15 +88,23 @@ __global__ void k_flow_upsample(const float* __restrict__ cu, const float* __res
     fv[o] = 2.0f * (tv * (1 - fy) + bv * fy);
 }
 
-// search_patch, flow.cpp:72-121. One thread per patch; z = direction.
-__global__ void __launch_bounds__(128) k_flow_patch(const float* __restrict__ from,
-                                                    const float* __restrict__ to0,
-                                                    const float* __restrict__ to1, int w, int h, int nx, int ny,
-                                                    const float* __restrict__ init_u_base,
-                                                    const float* __restrict__ init_v_base,
-                                                    size_t field_stride, float* __restrict__ res_base,
-                                                    size_t res_stride) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
+// search_patch, flow.cpp:72-121. One thread per patch; z = direction. The
+// template t and its gradients gx, gy (fixed for the 12 iterations) are kept
+// in shared memory ([n][thread], conflict-free) instead of 192 registers.
+constexpr int kPatchThreads = 64;
+
+__global__ void __launch_bounds__(kPatchThreads) k_flow_patch(const float* __restrict__ from,
+                                                              const float* __restrict__ to0,
+                                                              const float* __restrict__ to1, int w, int h, int nx,
+                                                              int ny, const float* __restrict__ init_u_base,
+                                                              const float* __restrict__ init_v_base,
+                                                              size_t field_stride, float* __restrict__ res_base,
+                                                              size_t res_stride) {
+    __shared__ float s_t[kPatch * kPatch * kPatchThreads];
+    __shared__ float s_gx[kPatch * kPatch * kPatchThreads];
+    __shared__ float s_gy[kPatch * kPatch * kPatchThreads];
+    const int tid = threadIdx.x;
+    int j = blockIdx.x * blockDim.x + tid;
     if (j >= nx * ny) return;
     const float* to = blockIdx.z ? to1 : to0;
     const float* iu = init_u_base + blockIdx.z * field_stride;
@@ -108,26 +116,23 @@ __global__ void __launch_bounds__(128) k_flow_patch(const float* __restrict__ fr
     const float seed_u = iu[static_cast<size_t>(cy) * w + cx];
     const float seed_v = iv[static_cast<size_t>(cy) * w + cx];
 
-    float t[kPatch * kPatch], gx[kPatch * kPatch], gy[kPatch * kPatch];
     double h00 = 1e-6, h01 = 0.0, h11 = 1e-6;
-#pragma unroll
-    for (int dy = 0; dy < kPatch; ++dy) {
-        int y = py + dy;
+#pragma unroll 8
+    for (int n = 0; n < kPatch * kPatch; ++n) {
+        int dy = n >> 3, dx = n & 7;
+        int y = py + dy, x = px + dx;
         int ym = max(y - 1, 0), yp = min(y + 1, h - 1);
-#pragma unroll
-        for (int dx = 0; dx < kPatch; ++dx) {
-            int n = dy * kPatch + dx;
-            int x = px + dx;
-            int xm = max(x - 1, 0), xp = min(x + 1, w - 1);
-            t[n] = __ldg(from + static_cast<size_t>(y) * w + x);
-            gx[n] = 0.5f * (__ldg(from + static_cast<size_t>(y) * w + xp) -
-                            __ldg(from + static_cast<size_t>(y) * w + xm));
-            gy[n] = 0.5f * (__ldg(from + static_cast<size_t>(yp) * w + x) -
-                            __ldg(from + static_cast<size_t>(ym) * w + x));
-            h00 += static_cast<double>(gx[n]) * gx[n];
-            h01 += static_cast<double>(gx[n]) * gy[n];
-            h11 += static_cast<double>(gy[n]) * gy[n];
-        }
+        int xm = max(x - 1, 0), xp = min(x + 1, w - 1);
+        const float* row = from + static_cast<size_t>(y) * w;
+        float t = __ldg(row + x);
+        float gx = 0.5f * (__ldg(row + xp) - __ldg(row + xm));
+        float gy = 0.5f * (__ldg(from + static_cast<size_t>(yp) * w + x) - __ldg(from + static_cast<size_t>(ym) * w + x));
+        s_t[n * kPatchThreads + tid] = t;
+        s_gx[n * kPatchThreads + tid] = gx;
+        s_gy[n * kPatchThreads + tid] = gy;
+        h00 += static_cast<double>(gx) * gx;
+        h01 += static_cast<double>(gx) * gy;
+        h11 += static_cast<double>(gy) * gy;
     }
     const double det = h00 * h11 - h01 * h01;
     const double inv00 = h11 / det, inv01 = -h01 / det, inv11 = h00 / det;
@@ -137,18 +142,15 @@ __global__ void __launch_bounds__(128) k_flow_patch(const float* __restrict__ fr
     const float fw = static_cast<float>(w), fh = static_cast<float>(h);
     for (int iter = 0; iter < kIters; ++iter) {
         double bu = 0.0, bv = 0.0, sse = 0.0;
-#pragma unroll
-        for (int dy = 0; dy < kPatch; ++dy) {
-#pragma unroll
-            for (int dx = 0; dx < kPatch; ++dx) {
-                int n = dy * kPatch + dx;
-                float sx = static_cast<float>(px + dx) + u;
-                float sy = static_cast<float>(py + dy) + v;
-                float r = sample_bilinear(to, w, h, sx, sy) - t[n];
-                bu += static_cast<double>(gx[n]) * r;
-                bv += static_cast<double>(gy[n]) * r;
-                sse += static_cast<double>(r) * r;
-            }
+#pragma unroll 16
+        for (int n = 0; n < kPatch * kPatch; ++n) {
+            int dy = n >> 3, dx = n & 7;
+            float sx = static_cast<float>(px + dx) + u;
+            float sy = static_cast<float>(py + dy) + v;
+            float r = sample_bilinear(to, w, h, sx, sy) - s_t[n * kPatchThreads + tid];
+            bu += static_cast<double>(s_gx[n * kPatchThreads + tid]) * r;
+            bv += static_cast<double>(s_gy[n * kPatchThreads + tid]) * r;
+            sse += static_cast<double>(r) * r;
         }
         mse = sse / (kPatch * kPatch);
         double step_u = inv00 * bu + inv01 * bv;
@@ -318,7 +320,7 @@ void compute_flow_multi(dco_ctx* ctx, const float* from, const float* const* to,
             cur ^= 1;
         }
         int np = L.nx * L.ny;
-        k_flow_patch<<<dim3(blocks_for(np, 128), 1, dirs), 128, 0, ctx->stream>>>(
+        k_flow_patch<<<dim3(blocks_for(np, kPatchThreads), 1, dirs), kPatchThreads, 0, ctx->stream>>>(
             p_from[l], p_to[0][l], dirs > 1 ? p_to[1][l] : p_to[0][l], L.w, L.h, L.nx, L.ny, U(cur, 0), V(cur, 0), fs, res,
             max_patches * 3);
         launched(ctx, "k_flow_patch");

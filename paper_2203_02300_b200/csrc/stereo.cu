@@ -162,6 +162,8 @@ __global__ void k_census(const float* __restrict__ img, int w, int h, int rw, in
 // compute_cost_volume, stereo.cpp:106-150. One thread per (pixel, d): the
 // warp spans consecutive d of one pixel, so the [p][d] store is coalesced and
 // the pixel's alpha/census/luminance loads are warp-uniform broadcasts.
+constexpr int kCostPix = 64;  // pixels of one row per cost-volume block
+
 struct CostParams {
     int w, h, nd, d_min, bits;
     double lambda_ad;
@@ -169,7 +171,7 @@ struct CostParams {
     double census[65];
 };
 
-__global__ void __launch_bounds__(256) k_cost_volume(const float* __restrict__ left,
+__global__ void __launch_bounds__(512) k_cost_volume(const float* __restrict__ left,
                                                      const float* __restrict__ right,
                                                      const uint64_t* __restrict__ cl,
                                                      const uint64_t* __restrict__ cr,
@@ -185,29 +187,36 @@ __global__ void __launch_bounds__(256) k_cost_volume(const float* __restrict__ l
     for (int i = threadIdx.x; i < 2 * DCO_EXP_TABLE_N; i += blockDim.x) s_exp[i] = g_exp_table[i];
     for (int i = threadIdx.x; i < 65; i += blockDim.x) s_census[i] = prm->census[i];
     __syncthreads();
+    // block = (32 lanes over d) x (blockDim.y pixels); a block walks kCostPix
+    // pixels of one row, so no per-element index division is needed.
     const int w = prm->w, nd = prm->nd;
-    const size_t total = static_cast<size_t>(w) * prm->h * nd;
-    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        size_t p = e / nd;
-        int k = static_cast<int>(e - p * nd);
-        int x = static_cast<int>(p % w);
-        int d = prm->d_min + k;
-        int qx = x - d;
-        float c;
-        if (qx < 0) {
-            c = 2.0f;
-        } else {
-            int m = min(min(armL[p], armR[p]), min(armU[p], armD[p]));
-            double alpha = prm->alpha[m];
-            size_t q = p - static_cast<size_t>(d);
-            float lum = left[p];
-            double c_ad = static_cast<double>(fabsf(lum - right[q])) * 255.0;
-            double ad_term = 1.0 - dco_exp(-c_ad / prm->lambda_ad, s_exp);
-            int hd = __popcll(cl[p] ^ cr[q]);
-            c = static_cast<float>(alpha * ad_term + (1.0 - alpha) * s_census[hd]);
+    const int y = blockIdx.y;
+    const int lane = threadIdx.x;
+    for (int xi = threadIdx.y; xi < kCostPix; xi += blockDim.y) {
+        const int x = blockIdx.x * kCostPix + xi;
+        if (x >= w) break;
+        const size_t p = static_cast<size_t>(y) * w + x;
+        const int m = min(min(armL[p], armR[p]), min(armU[p], armD[p]));
+        const double alpha = prm->alpha[m];
+        const double beta = 1.0 - alpha;
+        const float lum = left[p];
+        const uint64_t cp = cl[p];
+        float* dst = cost + p * nd;
+        for (int k = lane; k < nd; k += 32) {
+            const int d = prm->d_min + k;
+            const int qx = x - d;
+            float c;
+            if (qx < 0) {
+                c = 2.0f;
+            } else {
+                const size_t q = p - static_cast<size_t>(d);
+                double c_ad = static_cast<double>(fabsf(lum - right[q])) * 255.0;
+                double ad_term = 1.0 - dco_exp(-c_ad / prm->lambda_ad, s_exp);
+                int hd = __popcll(cp ^ cr[q]);
+                c = static_cast<float>(alpha * ad_term + beta * s_census[hd]);
+            }
+            dst[k] = c;
         }
-        cost[e] = c;
     }
 }
 
@@ -250,15 +259,44 @@ __global__ void k_agg_hpass(const float* __restrict__ cost, int w, int h, int nd
     const uint8_t* Rr = R + static_cast<size_t>(y) * w;
     double P = 0.0;
     ring[tid] = 0.0;
-    for (int x = 0; x < w; ++x) {
-        P += static_cast<double>(__ldg(src + static_cast<size_t>(x) * nd));
-        ring[((x + 1) & ring_mask) * stride + tid] = P;
-        int px = x + 1 - lag;
-        if (px >= 0) {
-            int a = px - Lr[px], b = px + Rr[px] + 1;
-            dst[static_cast<size_t>(px) * nd] =
-                ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
+    // software pipeline: the next kPF costs are in flight while the current
+    // kPF steps of the (inherently sequential) prefix chain execute
+    constexpr int kPF = 16;
+    float cur[kPF], nxt[kPF];
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) cur[j] = j < w ? __ldg(src + static_cast<size_t>(j) * nd) : 0.0f;
+    for (int x0 = 0; x0 < w; x0 += kPF) {
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            int x = x0 + kPF + j;
+            nxt[j] = x < w ? __ldg(src + static_cast<size_t>(x) * nd) : 0.0f;
         }
+        int la[kPF], ra[kPF];
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            int px = x0 + j + 1 - lag;
+            la[j] = ra[j] = 0;
+            if (px >= 0 && px < w) {
+                la[j] = __ldg(Lr + px);
+                ra[j] = __ldg(Rr + px);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            int x = x0 + j;
+            if (x < w) {
+                P += static_cast<double>(cur[j]);
+                ring[((x + 1) & ring_mask) * stride + tid] = P;
+                int px = x + 1 - lag;
+                if (px >= 0) {
+                    int a = px - la[j], b = px + ra[j] + 1;
+                    dst[static_cast<size_t>(px) * nd] =
+                        ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) cur[j] = nxt[j];
     }
     for (int px = max(w + 1 - lag, 0); px < w; ++px) {
         int a = px - Lr[px], b = px + Rr[px] + 1;
@@ -285,16 +323,45 @@ __global__ void k_agg_vpass(const double* __restrict__ hsum, int w, int h, int n
     float* dst = out + static_cast<size_t>(x) * nd + k;
     double C = 0.0;
     ring[tid] = 0.0;
-    for (int y = 0; y < h; ++y) {
-        C += __ldg(src + y * row);
-        ring[((y + 1) & ring_mask) * stride + tid] = C;
-        int py = y + 1 - lag;
-        if (py >= 0) {
-            size_t i = static_cast<size_t>(py) * w + x;
-            int a = py - U[i], b = py + D[i] + 1;
-            double total = ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
-            dst[py * row] = static_cast<float>(total / region[i]);
+    constexpr int kPF = 16;
+    double cur[kPF], nxt[kPF];
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) cur[j] = j < h ? __ldg(src + j * row) : 0.0;
+    for (int y0 = 0; y0 < h; y0 += kPF) {
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            int y = y0 + kPF + j;
+            nxt[j] = y < h ? __ldg(src + y * row) : 0.0;
         }
+        // the arms / region sizes of the kPF pixels finalised in this chunk
+        int ua[kPF], da[kPF], rg[kPF];
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            int py = y0 + j + 1 - lag;
+            ua[j] = da[j] = rg[j] = 1;
+            if (py >= 0 && py < h) {
+                size_t i = static_cast<size_t>(py) * w + x;
+                ua[j] = __ldg(U + i);
+                da[j] = __ldg(D + i);
+                rg[j] = __ldg(region + i);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            int y = y0 + j;
+            if (y < h) {
+                C += cur[j];
+                ring[((y + 1) & ring_mask) * stride + tid] = C;
+                int py = y + 1 - lag;
+                if (py >= 0) {
+                    int a = py - ua[j], b = py + da[j] + 1;
+                    double total = ring[(b & ring_mask) * stride + tid] - ring[(a & ring_mask) * stride + tid];
+                    dst[py * row] = static_cast<float>(total / rg[j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) cur[j] = nxt[j];
     }
     for (int py = max(h + 1 - lag, 0); py < h; ++py) {
         size_t i = static_cast<size_t>(py) * w + x;
@@ -355,79 +422,114 @@ __global__ void k_bin_max(const float* __restrict__ disp, int n, int* __restrict
     if ((threadIdx.x & 31) == 0 && b > 0) atomicMax(out, b);
 }
 
-// One warp per pixel, one lane per region row (rows beyond 32 loop); a
-// per-warp shared-memory histogram of nbins counters; mode = max count with
-// the smaller bin winning ties, as the reference's ascending scan does.
-__global__ void k_hist_refine(const float* __restrict__ cur, int w, int h,
-                              const uint8_t* __restrict__ L, const uint8_t* __restrict__ R,
-                              const uint8_t* __restrict__ U, const uint8_t* __restrict__ D,
-                              const int* __restrict__ bin_max_ptr, int nbins_cap,
-                              float* __restrict__ next) {
-    extern __shared__ unsigned hist_all[];
+// One warp per pixel (grid-stride over pixels). The cross region — the
+// horizontal spans of the pixels on the centre's vertical arm — is flattened
+// so all 32 lanes sample it in parallel; per 32 samples __match_any_sync
+// groups equal bins and one leader per distinct bin adds the group size to the
+// warp's shared-memory histogram (no atomics needed). Mode = max count, the
+// smaller bin winning ties, exactly the reference's ascending scan; only the
+// touched bin range is scanned and cleared.
+__global__ void __launch_bounds__(256) k_hist_refine(const float* __restrict__ cur, int w, int h,
+                                                     const uint8_t* __restrict__ L, const uint8_t* __restrict__ R,
+                                                     const uint8_t* __restrict__ U, const uint8_t* __restrict__ D,
+                                                     const int* __restrict__ bin_max_ptr, int nbins_cap, int rows_cap,
+                                                     float* __restrict__ next) {
+    extern __shared__ unsigned dyn[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned* hist = hist_all + static_cast<size_t>(warp) * nbins_cap;
+    const int per_warp = nbins_cap + 3 * rows_cap + 1;
+    unsigned* hist = dyn + static_cast<size_t>(warp) * per_warp;
+    int* roff = reinterpret_cast<int*>(hist + nbins_cap);  // rows_cap + 1 offsets
+    int* rx = roff + rows_cap + 1;                         // first column of each row span
+    int* ry = rx + rows_cap;                               // row index
     const int bin_max = *bin_max_ptr;
     const int nb = min(bin_max + 1, nbins_cap);
     for (int b = lane; b < nb; b += 32) hist[b] = 0u;
     __syncwarp();
-    const size_t p = (static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (p >= static_cast<size_t>(w) * h) return;
-    const float center = cur[p];
-    if (!isfinite(center)) {
-        if (lane == 0) next[p] = center;  // removed outliers stay removed
-        return;
-    }
-    const int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
-    const int up = U[p], dn = D[p];
-    int count = 0, lo = bin_max, hi = 0;
-    for (int r = -up + lane; r <= dn; r += 32) {
-        int vy = y + r;
-        size_t vi = static_cast<size_t>(vy) * w + x;
-        const float* row = cur + static_cast<size_t>(vy) * w;
-        for (int c = -static_cast<int>(L[vi]); c <= static_cast<int>(R[vi]); ++c) {
-            float v = row[x + c];
-            if (!isfinite(v)) continue;
-            int bin = static_cast<int>(lroundf(v));
-            bin = min(max(bin, 0), nb - 1);
-            atomicAdd(&hist[bin], 1u);
-            ++count;
-            lo = min(lo, bin);
-            hi = max(hi, bin);
+    const size_t npix = static_cast<size_t>(w) * h;
+    const size_t nwarps = static_cast<size_t>(gridDim.x) * (blockDim.x >> 5);
+    for (size_t p = static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp; p < npix; p += nwarps) {
+        const float center = cur[p];
+        if (!isfinite(center)) {
+            if (lane == 0) next[p] = center;  // removed outliers stay removed
+            continue;
         }
-    }
+        const int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
+        const int up = U[p], nrows = up + D[p] + 1;
+        // row spans and their exclusive prefix (flattened offsets)
+        int total = 0;
+        for (int rb = 0; rb < nrows; rb += 32) {
+            int r = rb + lane, len = 0;
+            if (r < nrows) {
+                int vy = y - up + r;
+                size_t vi = static_cast<size_t>(vy) * w + x;
+                int l = L[vi];
+                len = l + R[vi] + 1;
+                rx[r] = x - l;
+                ry[r] = vy;
+            }
+            int inc = len;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        count += __shfl_xor_sync(0xffffffffu, count, off);
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, off));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, off));
-    }
-    __syncwarp();
-    int best_c = 0, best_b = lo;
-    for (int b = lo + lane; b <= hi; b += 32) {
-        int cnt = static_cast<int>(hist[b]);
-        if (cnt > best_c) {  // ascending within the lane: first max kept
-            best_c = cnt;
-            best_b = b;
+            for (int off = 1; off < 32; off <<= 1) {
+                int o = __shfl_up_sync(0xffffffffu, inc, off);
+                if (lane >= off) inc += o;
+            }
+            if (r < nrows) roff[r] = total + inc - len;
+            total += __shfl_sync(0xffffffffu, inc, 31);
         }
-    }
+        if (lane == 0) roff[nrows] = total;
+        __syncwarp();
+        int count = 0, lo = bin_max, hi = 0, row = 0;
+        for (int f0 = 0; f0 < total; f0 += 32) {
+            int f = f0 + lane;
+            int bin = -1;
+            if (f < total) {
+                while (roff[row + 1] <= f) ++row;
+                float v = cur[static_cast<size_t>(ry[row]) * w + rx[row] + (f - roff[row])];
+                if (isfinite(v)) {
+                    bin = min(max(static_cast<int>(lroundf(v)), 0), nb - 1);
+                    ++count;
+                    lo = min(lo, bin);
+                    hi = max(hi, bin);
+                }
+            }
+            unsigned grp = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && lane == __ffs(grp) - 1) hist[bin] += __popc(grp);
+            __syncwarp();
+        }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        int oc = __shfl_xor_sync(0xffffffffu, best_c, off);
-        int ob = __shfl_xor_sync(0xffffffffu, best_b, off);
-        if (oc > best_c || (oc == best_c && ob < best_b)) {
-            best_c = oc;
-            best_b = ob;
+        for (int off = 16; off > 0; off >>= 1) {
+            count += __shfl_xor_sync(0xffffffffu, count, off);
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, off));
         }
-    }
-    if (lane == 0) {
-        if (best_c == 1 && count >= 4)
-            next[p] = __int_as_float(0x7fc00000);  // quiet NaN nodata
-        else
-            next[p] = static_cast<float>(best_c > 0 ? best_b : lo);
+        int best_c = 0, best_b = lo;
+        for (int b = lo + lane; b <= hi; b += 32) {
+            int cnt = static_cast<int>(hist[b]);
+            hist[b] = 0u;
+            if (cnt > best_c) {
+                best_c = cnt;
+                best_b = b;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            int oc = __shfl_xor_sync(0xffffffffu, best_c, off);
+            int ob = __shfl_xor_sync(0xffffffffu, best_b, off);
+            if (oc > best_c || (oc == best_c && ob < best_b)) {
+                best_c = oc;
+                best_b = ob;
+            }
+        }
+        if (lane == 0) {
+            if (best_c == 1 && count >= 4)
+                next[p] = __int_as_float(0x7fc00000);  // quiet NaN nodata
+            else
+                next[p] = static_cast<float>(best_b);
+        }
+        __syncwarp();
     }
 }
 
-// Clears the per-warp histograms is done at kernel start; nothing persists.
 
 // -------------------------------------------------------- sparse depth -----
 // disparity_to_sparse_depth, stereo.cpp:301-315.
@@ -548,11 +650,9 @@ void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, in
     make_stereo_tables(cfg, &t);
     for (int i = 0; i < 256; ++i) hp.alpha[i] = t.alpha[i];
     for (int i = 0; i < 65; ++i) hp.census[i] = t.census[i];
-    const size_t total = n * hp.nd;
-    int dev_sms = 148;
-    unsigned blocks = static_cast<unsigned>(std::min<size_t>(blocks_for(total, 256), dev_sms * 16));
-    k_cost_volume<<<blocks, 256, 0, ctx->stream>>>(left, right, census, census + n, l, r, u, d, hp,
-                                                   cost);
+    dim3 grid((w + kCostPix - 1) / kCostPix, h);
+    k_cost_volume<<<grid, dim3(32, 16), 0, ctx->stream>>>(left, right, census, census + n, l, r, u, d, hp,
+                                                           cost);
     launched(ctx, "k_cost_volume");
 }
 
@@ -596,7 +696,7 @@ void select_disparity_wta(dco_ctx* ctx, const float* cost, int w, int h, int d_m
 
 void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
                                 const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters,
-                                int bin_bound, float* out) {
+                                int bin_bound, int max_arm, float* out) {
     const size_t n = static_cast<size_t>(w) * h;
     require(iters >= 0, "refine_disparity_histogram: negative iteration count");
     if (iters == 0) {
@@ -617,7 +717,8 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     require(cap <= 8192, "refine_disparity_histogram: disparities above 8191 are not supported");
     cap = (cap + 31) & ~31;
     const int warps = 8;
-    size_t smem = static_cast<size_t>(warps) * cap * sizeof(unsigned);
+    const int rows_cap = 2 * max_arm + 2;
+    size_t smem = static_cast<size_t>(warps) * (cap + 3 * rows_cap + 1) * sizeof(unsigned);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_hist_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -626,10 +727,10 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     float* bufs[2] = {static_cast<float*>(scratch(ctx, S_DISP0, n * 4)),
                       static_cast<float*>(scratch(ctx, S_DISP1, n * 4))};
     const float* src = disp;
+    const unsigned blocks = static_cast<unsigned>(std::min<size_t>(blocks_for(n, warps), 148 * 16));
     for (int it = 0; it < iters; ++it) {
         float* dst = (it == iters - 1) ? out : bufs[it & 1];
-        k_hist_refine<<<blocks_for(n * 32, warps * 32), warps * 32, smem, ctx->stream>>>(
-            src, w, h, l, r, u, d, bmax, cap, dst);
+        k_hist_refine<<<blocks, warps * 32, smem, ctx->stream>>>(src, w, h, l, r, u, d, bmax, cap, rows_cap, dst);
         launched(ctx, "k_hist_refine");
         src = dst;
     }
@@ -696,7 +797,7 @@ int dco_select_disparity_wta(dco_ctx* ctx, const float* cost, int w, int h, int 
 int dco_refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
                                    const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters,
                                    float* out) {
-    return guarded(ctx, [&] { refine_disparity_histogram(ctx, disp, w, h, l, r, u, d, iters, -1, out); });
+    return guarded(ctx, [&] { refine_disparity_histogram(ctx, disp, w, h, l, r, u, d, iters, -1, max_arm_length(ctx, l, r, u, d, w, h), out); });
 }
 
 int dco_disparity_to_sparse_depth(dco_ctx* ctx, const float* disp, int w, int h, const dco_config* cfg,

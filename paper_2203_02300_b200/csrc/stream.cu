@@ -26,7 +26,7 @@ void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, cons
 void select_disparity_wta(dco_ctx* ctx, const float* cost, int w, int h, int d_min, int nd, float* disp);
 void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
                                 const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters, int bin_bound,
-                                float* out);
+                                int max_arm, float* out);
 void disparity_to_sparse_depth(dco_ctx* ctx, const float* disp, int w, int h, const dco_config* cfg, int fw,
                                int fh, float* out);
 void compute_flow_multi(dco_ctx* ctx, const float* from, const float* const* to, int dirs, int w, int h,
@@ -230,7 +230,7 @@ void run_frame(dco_stream* s, dco_frame_result* res) {
     select_disparity_wta(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
     s->mark(DCO_SPAN_WTA + 1);
     refine_disparity_histogram(ctx, s->disp_wta, qw, qh, L, R, U, D, cfg->hist_iterations, cfg->d_max,
-                               s->disparity);
+                               cfg->cross_arm_l1, s->disparity);
     s->mark(DCO_SPAN_REFINE + 1);
     disparity_to_sparse_depth(ctx, s->disparity, qw, qh, cfg, fw, fh, s->sparse);
     s->mark(DCO_SPAN_SPARSE + 1);
@@ -569,7 +569,7 @@ int dco_stereo_sparse_depth(dco_ctx* ctx, const float* left_q, const float* righ
         aggregate_costs(ctx, cost, w, h, nd, L, R, U, D, cfg->cross_arm_l1, agg);
         select_disparity_wta(ctx, agg, w, h, cfg->d_min, nd, d0);
         float* disp = disparity ? disparity : d1;
-        refine_disparity_histogram(ctx, d0, w, h, L, R, U, D, cfg->hist_iterations, cfg->d_max, disp);
+        refine_disparity_histogram(ctx, d0, w, h, L, R, U, D, cfg->hist_iterations, cfg->d_max, cfg->cross_arm_l1, disp);
         disparity_to_sparse_depth(ctx, disp, w, h, cfg, fw, fh, sparse);
     });
 }
