@@ -2,7 +2,7 @@
  * dco_gpu.h — C-ABI of the B200-native depth-contour-occlusion (DCO) hot path.
  *
  * Every entry point below replaces one free function of the reference's L2
- * stage API (namespace dco, /root/reference/proj/include/dco/*.hpp). The
+ * stage API (namespace dco, /root/reference/proj/include/dco/ *.hpp). The
  * mapping is one-to-one and cited per function. Differences are mechanical:
  *   - plain pointers + sizes instead of std::vector-owning structs;
  *   - stage inputs/outputs are DEVICE pointers owned by the caller (cudaMalloc
