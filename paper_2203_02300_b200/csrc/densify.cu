@@ -349,6 +349,7 @@ struct CGArgs {
     const int* fallback_valid;  // nullable: fallback usable only when *fallback_valid
     SolveOut* out;
     int mode;  // experiment knobs (0 in production): 1 no in-loop grid sync, 2 no halo loads, 4 no prec load
+    long long* dbg;  // optional per-phase clock64 stamps of block 0 (DCO_PCG_DEBUG)
 };
 
 // Sum of the per-block partials, identical in every block (same order).
@@ -623,17 +624,96 @@ __device__ __forceinline__ void grid_reduce(const double* part, int stride, int 
     }
 }
 
+// Grid-wide deterministic all-reduce fused with the grid barrier: every block
+// publishes its partial row and arrives on a counter; the LAST block to
+// arrive sums all rows in block order (fixed, so every run and every block
+// sees identical bits), publishes the totals and releases the others. One
+// barrier instead of "grid.sync + every block re-reading every partial".
+struct GridBar {
+    unsigned count;
+    unsigned gen;
+    unsigned pad[30];
+    double result[2][8];
+};
+
+template <int K>
+__device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, double* partials, unsigned& gen,
+                                               double* sm, int* sm_flag, double (&res)[K]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nb = gridDim.x;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sm[warp * K + k] = v[k];
+    __syncthreads();
+    if (warp == 0) {
+        double bs[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = lane < nw ? sm[lane * K + k] : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            bs[k] = s;
+        }
+        unsigned arrived = 0;
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) __stcg(partials + blockIdx.x * 8 + k, bs[k]);
+            // release my partial row, acquire everyone's (acq_rel RMW)
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(&bar->count) : "memory");
+        }
+        arrived = __shfl_sync(0xffffffffu, arrived, 0);
+        const int slot = gen & 1u;
+        if (arrived == static_cast<unsigned>(nb) - 1u) {
+            // last arrival: all rows are visible; sum them in block order
+            double acc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = 0.0;
+            for (int b = lane; b < nb; b += 32)
+#pragma unroll
+                for (int k = 0; k < K; ++k) acc[k] += __ldcg(partials + b * 8 + k);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double s = acc[k];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                if (lane == 0) {
+                    __stcg(&bar->result[slot][k], s);
+                    sm[k] = s;
+                }
+            }
+            if (lane == 0) {
+                bar->count = 0u;
+                asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&bar->gen), "r"(gen + 1u) : "memory");
+            }
+        } else if (lane == 0) {
+            unsigned g;
+            do {
+                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(&bar->gen) : "memory");
+            } while (g == gen);
+#pragma unroll
+            for (int k = 0; k < K; ++k) sm[k] = __ldcg(&bar->result[slot][k]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) res[k] = sm[k];
+    ++gen;
+    __syncthreads();  // sm reused by the next reduction
+}
+
 template <int EPT, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) {
-    // Block b owns [base, base + size): sizes differ by at most one, and every
-    // block holds >= (EPT-1)*1024 unknowns, so only the last register slot of
-    // a thread can be empty. Solver arithmetic uses explicit FMAs: the solve
-    // is tolerance-matched (not bit-exact) anyway and this halves the FP64
-    // instruction count.
-    cg::grid_group grid = cg::this_grid();
+__global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, GridBar* bar) {
+    // Block b owns [base, base + size): sizes differ by at most one. r and p
+    // in registers, x / xs / rs / (q then z) in shared memory, p published to
+    // a global halo copy for the SpMV. Solver arithmetic uses explicit FMAs:
+    // the solve is tolerance-matched (not bit-exact), which halves FP64 work.
     extern __shared__ double sx[];  // [4][chunk]: x, xs, rs, qz
-    __shared__ double sm_part[32 * 5];
-    __shared__ double sm_res[3][32 * 5];
+    __shared__ double sm[32 * 5];
+    __shared__ int sm_flag;
     const int w = a.w, h = a.h;
     const int n = static_cast<int>(a.n);
     const int nb = gridDim.x;
@@ -641,8 +721,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
     const int base = blockIdx.x * q + min(static_cast<int>(blockIdx.x), rem);
     const int size = q + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
     const int t = threadIdx.x;
-    // register slots of this thread that hold an unknown (EPT may be rounded up)
-    const int nv = size > t ? (size - t + THREADS - 1) / THREADS : 0;
+    const int nv = size > t ? (size - t + THREADS - 1) / THREADS : 0;  // occupied register slots
     double* s_x = sx + t;
     double* s_xs = sx + chunk + t;
     double* s_rs = sx + 2 * chunk + t;
@@ -650,13 +729,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
     const double* __restrict__ diag = a.diag + base + t;
     const double* __restrict__ ch = a.ch + base + t;
     const double* __restrict__ cv = a.cv + base + t;
-    double* pg = a.p + base + t;  // global halo copy of p
+    double* pg = a.p + base + t;
     const double* __restrict__ prec = a.prec + base + t;
-    double* part_setup = a.part;
-    double* part_pq = a.part + 8 * nb;
-    double* part_rho = a.part + 16 * nb;
-    double* part_rs = a.part + 24 * nb;
-    double* part_obj = a.part + 32 * nb;
+    unsigned gen = *reinterpret_cast<volatile unsigned*>(&bar->gen);
     double r[EPT], p[EPT];
     uint64_t nbr = 0;  // 4 bits per slot (EPT <= 16): 1 right, 2 left, 4 down, 8 up
 #define DCO_OK(k) ((k) < nv)
@@ -665,8 +740,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
     unsigned long long anchors = a.anchors_dev ? *a.anchors_dev : a.anchors_host;
     if (anchors == 0) {
         const float* fb = (a.fallback && (!a.fallback_valid || *a.fallback_valid)) ? a.fallback : nullptr;
-        for (int i = base + t; i < base + size; i += THREADS)
-            a.dense[i] = fb ? fb[i] : __int_as_float(0x7fc00000);
+        for (int i = base + t; i < base + size; i += THREADS) a.dense[i] = fb ? fb[i] : __int_as_float(0x7fc00000);
         if (blockIdx.x == 0 && t == 0) {
             a.out->status = 3;
             a.out->iterations = 0;
@@ -676,8 +750,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
     const double cterm = a.constant_term_dev ? *a.constant_term_dev : a.constant_term_host;
 
     // setup (densify.cpp:147-166): x = initial, r = b - A x, z = M r, p = z
+    double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // b.b, r.r, r.z, x.Ax, b.x
     {
-        double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // b.b, r.r, r.z, x.Ax, b.x
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
             r[k] = 0.0;
@@ -701,18 +775,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
                 r[k] = ri;
                 p[k] = zi;
                 a.p[i] = zi;
-                v[0] += b * b;
-                v[1] += ri * ri;
-                v[2] += ri * zi;
-                v[3] += xi * ax;
-                v[4] += b * xi;
+                tot[0] += b * b;
+                tot[1] += ri * ri;
+                tot[2] += ri * zi;
+                tot[3] += xi * ax;
+                tot[4] += b * xi;
             }
         }
-        block_partial<5>(v, sm_part, part_setup + 8 * blockIdx.x);
+        barrier_reduce<5>(tot, bar, a.part, gen, sm, &sm_flag, tot);
     }
-    grid.sync();
-    double tot[5];
-    grid_reduce<5>(part_setup, 8, nb, tot, sm_res[0]);
     const double bnorm = sqrt(tot[0]);
     const double denom = bnorm > 0.0 ? bnorm : 1.0;
     double snorm = sqrt(tot[1]);
@@ -723,34 +794,39 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
     }
 
     int iter = 0;
+#define STAMP(j)                                                                                      \
+    if (a.dbg && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && t == 0 && iter < 64) \
+        a.dbg[(blockIdx.x ? 640 : 0) + iter * 10 + (j)] = clock64();
     while (iter < a.max_iter && snorm / denom > a.tol) {
+        STAMP(0)
         // A: q = A p (halo p from global), pq -- stencil order of densify.cpp:125-129
+        double pq;
         {
-            double v = 0.0;
+            double v[1] = {0.0};
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 if (DCO_OK(k)) {
                     const unsigned m = static_cast<unsigned>(nbr >> (4 * k));
                     const int o = KO(k);
                     double acc = diag[o] * p[k];
-                    if (m & 1u) acc = __fma_rn(-ch[o], pg[o + 1], acc);
-                    if (m & 2u) acc = __fma_rn(-ch[o - 1], pg[o - 1], acc);
-                    if (m & 4u) acc = __fma_rn(-cv[o], pg[o + w], acc);
-                    if (m & 8u) acc = __fma_rn(-cv[o - w], pg[o - w], acc);
+                    if (m & 1u) acc = __fma_rn(-ch[o], __ldcg(pg + o + 1), acc);
+                    if (m & 2u) acc = __fma_rn(-ch[o - 1], __ldcg(pg + o - 1), acc);
+                    if (m & 4u) acc = __fma_rn(-cv[o], __ldcg(pg + o + w), acc);
+                    if (m & 8u) acc = __fma_rn(-cv[o - w], __ldcg(pg + o - w), acc);
                     s_qz[o] = acc;
-                    v = __fma_rn(p[k], acc, v);
+                    v[0] = __fma_rn(p[k], acc, v[0]);
                 }
             }
-            double vv[1] = {v};
-            block_partial<1>(vv, sm_part, part_pq + 8 * blockIdx.x);
+            STAMP(1)
+            double res[1];
+            barrier_reduce<1>(v, bar, a.part, gen, sm, &sm_flag, res);
+            pq = res[0];
+            STAMP(2)
         }
-        grid.sync();
-        double pqv[1];
-        grid_reduce<1>(part_pq, 8, nb, pqv, sm_res[1]);
-        const double pq = pqv[0];
         if (pq <= 0.0) break;  // uniform across the grid
         const double alpha = rho / pq;
         // B: x, r, z; rho_next; MR numerators
+        double rho_next, sd, dd;
         {
             double v[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -769,12 +845,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
                     v[2] = __fma_rn(di, di, v[2]);
                 }
             }
-            block_partial<3>(v, sm_part, part_rho + 8 * blockIdx.x);
+            STAMP(3)
+            double res[3];
+            barrier_reduce<3>(v, bar, a.part, gen, sm, &sm_flag, res);
+            rho_next = res[0];
+            sd = res[1];
+            dd = res[2];
+            STAMP(4)
         }
-        grid.sync();
-        double s3[3];
-        grid_reduce<3>(part_rho, 8, nb, s3, sm_res[2]);
-        const double rho_next = s3[0], sd = s3[1], dd = s3[2];
         const double beta = rho_next / rho;
         rho = rho_next;
         double eta = 0.0;
@@ -784,46 +862,34 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
         }
         // C: p = z + beta p (published for the next SpMV), MR smoothing, |rs|^2
         {
-            double v = 0.0;
-            if (eta > 0.0) {
+            double v[1] = {0.0};
 #pragma unroll
-                for (int k = 0; k < EPT; ++k) {
-                    if (DCO_OK(k)) {
-                        const int o = KO(k);
-                        double pn = __fma_rn(beta, p[k], s_qz[o]);
-                        p[k] = pn;
-                        pg[o] = pn;
-                        double rsi = s_rs[o];
+            for (int k = 0; k < EPT; ++k) {
+                if (DCO_OK(k)) {
+                    const int o = KO(k);
+                    double pn = __fma_rn(beta, p[k], s_qz[o]);
+                    p[k] = pn;
+                    __stcg(pg + o, pn);
+                    double rsi = s_rs[o];
+                    if (eta > 0.0) {
                         rsi = __fma_rn(eta, r[k] - rsi, rsi);
                         s_rs[o] = rsi;
                         double xsi = s_xs[o];
                         s_xs[o] = __fma_rn(eta, s_x[o] - xsi, xsi);
-                        v = __fma_rn(rsi, rsi, v);
                     }
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < EPT; ++k) {
-                    if (DCO_OK(k)) {
-                        const int o = KO(k);
-                        double pn = __fma_rn(beta, p[k], s_qz[o]);
-                        p[k] = pn;
-                        pg[o] = pn;
-                        double rsi = s_rs[o];
-                        v = __fma_rn(rsi, rsi, v);
-                    }
+                    v[0] = __fma_rn(rsi, rsi, v[0]);
                 }
             }
-            double vv[1] = {v};
-            block_partial<1>(vv, sm_part, part_rs + 8 * blockIdx.x);
+            STAMP(5)
+            double res[1];
+            barrier_reduce<1>(v, bar, a.part, gen, sm, &sm_flag, res);  // also publishes p (halo)
+            snorm = sqrt(res[0]);
+            STAMP(6)
         }
-        grid.sync();
-        double sn[1];
-        grid_reduce<1>(part_rs, 8, nb, sn, sm_res[0]);
-        snorm = sqrt(sn[0]);
         ++iter;
         if (blockIdx.x == 0 && t == 0 && iter < a.hist_cap) a.hist[iter] = snorm;
     }
+#undef STAMP
 #undef DCO_OK
 #undef KO
     // publish xs for the final objective's stencil, dense map
@@ -832,36 +898,33 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk) 
         a.xs[i] = xsi;
         a.dense[i] = static_cast<float>(dmax0(xsi));
     }
-    grid.sync();
     {
-        double v[2] = {0.0, 0.0};
-        for (int i = base + t; i < base + size; i += THREADS) {
-            int xx = i % w, y = i / w;
-            double xsi = a.xs[i];
-            v[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
-            v[1] += a.rhs[i] * xsi;
-        }
-        block_partial<2>(v, sm_part, part_obj + 8 * blockIdx.x);
+        double z[1] = {0.0}, dummy[1];
+        barrier_reduce<1>(z, bar, a.part, gen, sm, &sm_flag, dummy);  // xs visible grid-wide
     }
-    grid.sync();
-    if (blockIdx.x == 0) {
-        double o[2];
-        grid_reduce<2>(part_obj, 8, nb, o, sm_res[1]);
-        if (t == 0) {
-            a.out->objective_final = o[0] - 2.0 * o[1] + cterm;
-            a.out->status = 0;
-            a.out->iterations = iter;
-            a.out->relative_residual = snorm / denom;
-        }
+    double o[2] = {0.0, 0.0};
+    for (int i = base + t; i < base + size; i += THREADS) {
+        int xx = i % w, y = i / w;
+        double xsi = __ldcg(a.xs + i);
+        o[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
+        o[1] += a.rhs[i] * xsi;
+    }
+    barrier_reduce<2>(o, bar, a.part, gen, sm, &sm_flag, o);
+    if (blockIdx.x == 0 && t == 0) {
+        a.out->objective_final = o[0] - 2.0 * o[1] + cterm;
+        a.out->status = 0;
+        a.out->iterations = iter;
+        a.out->relative_residual = snorm / denom;
     }
 }
 
 inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
 
 int g_pcg_blocks = 0;
+long long* g_pcg_dbg = nullptr;
 int g_sms = 0;
 
-typedef void (*OnchipKernel)(CGArgs, int);
+typedef void (*OnchipKernel)(CGArgs, int, GridBar*);
 constexpr int kOnchipThreadsUsed = 1024;
 OnchipKernel onchip_for(int ept, int* ept_used) {
     *ept_used = ept;
@@ -984,6 +1047,13 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     a.fallback_valid = fallback_valid;
     a.out = static_cast<SolveOut*>(out_dev);
     a.mode = getenv("DCO_PCG_MODE") ? atoi(getenv("DCO_PCG_MODE")) : 0;
+    a.dbg = nullptr;
+    if (getenv("DCO_PCG_DEBUG")) {
+        static long long* dbg = nullptr;
+        if (!dbg) cuda_check(cudaMalloc(&dbg, 1280 * sizeof(long long)), "dbg");
+        a.dbg = dbg;
+        g_pcg_dbg = dbg;
+    }
     // on-chip resident path: one 1024-thread block per SM, chunk of unknowns
     // per block with 4 doubles each in shared memory, <= 8 per thread
     const int sms = g_sms ? g_sms : (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, ctx->device), g_sms);
@@ -1000,7 +1070,9 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
             attr[ept] = true;
         }
         int chunk_arg = chunk;
-        void* params[] = {&a, &chunk_arg};
+        GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
+        cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
+        void* params[] = {&a, &chunk_arg, &bar};
         cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(sms), dim3(kOnchipThreadsUsed),
                                                params, smem, ctx->stream),
                    "launch k_pcg_onchip");
@@ -1031,6 +1103,13 @@ void read_solve_out(const void* host, int* status, int* iters, double* relres, d
 using namespace dco_gpu;
 
 extern "C" {
+
+// debug: copies the last solve's per-phase clock64 stamps (DCO_PCG_DEBUG)
+__attribute__((visibility("default"))) int dco_debug_pcg_stamps(long long* host, int n) {
+    if (!g_pcg_dbg) return 1;
+    cudaDeviceSynchronize();
+    return cudaMemcpy(host, g_pcg_dbg, n * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 4;
+}
 
 int dco_smoothness_weight(dco_ctx* ctx, int px, int py, int qx, int qy, const uint8_t* edges, int w,
                           int h, const float* mf, int qw, int qh, const float* mi, double* out) {
