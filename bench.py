@@ -9,11 +9,12 @@ virtual layer — the body of run_pipeline (reference src/pipeline.cpp:183-258).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One process per GPU (torchrun for N>1); every rank runs its own stream
-(frames shard across GPUs, no data-path collective: "scaling": "weak"). The
-timed region is bracketed by a barrier + cuda.synchronize; the reported time
-is the max over ranks. L2 is flushed (256 MiB memset) between timed steps,
-outside each step's event pair.
+One process per GPU (torchrun for N>1); every rank runs --streams independent
+pipeline streams concurrently (own dco_ctx + CUDA stream each; frames shard
+across streams and GPUs, no data-path collective: "scaling": "weak"). A step
+is one frame on every stream. The timed region is bracketed by a barrier +
+cuda.synchronize; the reported time is the max over ranks. L2 is flushed
+(256 MiB memset) before every frame inside the timed region (conservative).
 
 `value` times frames whose u8 inputs are already in HBM. `e2e` times the same
 steps through the host-buffer C-ABI (dco_stream_push_gray8_host): pinned u8
@@ -59,7 +60,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -120,6 +121,18 @@ def cpu_reference_frames(frames, d_pre_list, cfg_dict, procs):
         return time.perf_counter() - t0
 
 
+def cpu_procs():
+    """All host threads, bounded by memory (~0.7 GB per reference process)."""
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+
+        n = max(1, min(n, int(psutil.virtual_memory().available / 0.7e9)))
+    except Exception:
+        pass
+    return n
+
+
 def _cpu_warm(_):
     from oracle import ref
 
@@ -175,7 +188,7 @@ def run_reference(args, world, rank):
     out = ref.pipeline_frame(q[0], q[1], q[2], f(frames[0][1]), ref.downsample_half(f(frames[0][3])),
                              np.repeat(f(frames[0][1])[:, :, None], 3, 2), None, _VIRT[0], _VIRT[1], cfg)
     d_pre = [out["dense"]]
-    procs = min(os.cpu_count() or 1, 8)
+    procs = cpu_procs()
     times = []
     for it in range(args.warmup + args.steps):
         t = cpu_reference_frames(frames, d_pre, cfg.as_dict(), procs)
@@ -211,6 +224,8 @@ def algorithmic_bytes(span, iters):
 
 
 def run_ours(args, world, rank, local):
+    import threading as th
+
     import numpy as np
     import torch
 
@@ -229,89 +244,112 @@ def run_ours(args, world, rank, local):
     from paper_2203_02300_b200.config import Config
     from paper_2203_02300_b200.synth import StereoVideo
 
+    S = args.streams
     cfg = Config(d_max=D - 1)
-    vid = StereoVideo(W, H, seed=61 + rank)
     nframes = 32
-    lefts, rights = zip(*[vid.frame(i) for i in range(nframes)])
-    dev_l = torch.from_numpy(np.stack(lefts)).cuda()
-    dev_r = torch.from_numpy(np.stack(rights)).cuda()
-    # virtual layer: a depth-tested cube (render_virtual is outside the path;
-    # a fixed synthetic layer stands in: a box at 1.5 m in the image centre)
+    vids = [StereoVideo(W, H, seed=61 + 97 * rank + s) for s in range(S)]
+    host = [[v.frame(i) for i in range(nframes)] for v in vids]
+    dev_l = [torch.from_numpy(np.stack([f[0] for f in h])).cuda() for h in host]
+    dev_r = [torch.from_numpy(np.stack([f[1] for f in h])).cuda() for h in host]
+    # virtual layer: render_virtual is outside the path; a fixed synthetic
+    # layer stands in (a box at 1.5 m over the image centre)
     vdepth = torch.full((H, W), float("nan"), device="cuda")
     vrgb = torch.zeros((H, W, 3), device="cuda")
     vdepth[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = 1.5
     vrgb[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = torch.tensor([1.0, 0.55, 0.1], device="cuda")
 
-    s = dco.Stream(W, H, cfg)
-    s.set_virtual(vrgb, vdepth)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    stream = torch.cuda.current_stream()
-    i = 0
-    # fill the window and reach steady state (d_pre chain) + W warmups
+    tstreams = [torch.cuda.Stream() for _ in range(S)]
+    streams = []
+    for s in range(S):
+        with torch.cuda.stream(tstreams[s]):
+            st = dco.Stream(W, H, cfg, ctx=dco.new_context(tstreams[s]))
+            st.set_virtual(vrgb, vdepth)
+            streams.append(st)
+    flush = [torch.empty(256 << 20, dtype=torch.uint8, device="cuda") for _ in range(S)]
+    pos = [0] * S
+
+    def push(s, want=False):
+        with torch.cuda.stream(tstreams[s]):
+            flush[s].zero_()  # L2 flush before every frame, inside the timed region
+            r = streams[s].push_gray8(dev_l[s][pos[s] % nframes], dev_r[s][pos[s] % nframes], want_result=want)
+        pos[s] += 1
+        return r
+
+    # fill each window (3 frames), reach the d_pre steady state, then W warm-ups
     for _ in range(3 + args.warmup):
-        s.push_gray8(dev_l[i % nframes], dev_r[i % nframes], want_result=False)
-        i += 1
+        for s in range(S):
+            push(s)
     torch.cuda.synchronize()
-    s.set_timing(True)
-    launches0 = dco.kernel_launches()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    iters = []
+    launches0 = sum(st.launches() for st in streams)
+    main = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()
-            ev[k][0].record(stream)
-            s.push_gray8(dev_l[i % nframes], dev_r[i % nframes], want_result=False)
-            ev[k][1].record(stream)
-            i += 1
+        t0.record(main)
+        for ts in tstreams:
+            ts.wait_event(t0)
+        for _ in range(args.steps):
+            for s in range(S):
+                push(s)
+        for ts in tstreams:
+            e = torch.cuda.Event()
+            e.record(ts)
+            main.wait_event(e)
+        t1.record(main)
         torch.cuda.synchronize()
         barrier()
-    launches = dco.kernel_launches() - launches0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    spans, nt = s.span_times()
-    s.set_timing(False)
-    # solver iterations of the timed frames (one extra pushed frame reports it)
-    res = s.push_gray8(dev_l[i % nframes], dev_r[i % nframes])
-    i += 1
-    iters = res.densify_iterations
+    total_ms = t0.elapsed_time(t1)
+    launches = sum(st.launches() for st in streams) - launches0
+    iters = push(0, want=True).densify_iterations
 
-    # end to end: host pinned u8 in, composite/mask/dense out, per step
-    h_l = [torch.from_numpy(a).pin_memory() for a in lefts]
-    h_r = [torch.from_numpy(a).pin_memory() for a in rights]
-    comp = torch.empty((H, W, 3), dtype=torch.float32).pin_memory()
-    mask = torch.empty((H, W), dtype=torch.uint8).pin_memory()
-    dense = torch.empty((H, W), dtype=torch.float32).pin_memory()
-    for _ in range(2):
-        s.push_gray8_host(h_l[i % nframes], h_r[i % nframes], comp, mask, dense)
-        i += 1
-    e2e_ms = []
+    # isolated per-span timing (one stream, nothing concurrent) for the roofline
+    streams[0].set_timing(True)
+    for _ in range(5):
+        push(0)
+    torch.cuda.synchronize()
+    spans, nt = streams[0].span_times()
+    streams[0].set_timing(False)
+
+    # end to end through the host-buffer C-ABI: pinned u8 in, composite/mask/
+    # dense out, S host threads (ctypes releases the GIL) driving S contexts
+    hl = [[torch.from_numpy(f[0]).pin_memory() for f in h] for h in host]
+    hr = [[torch.from_numpy(f[1]).pin_memory() for f in h] for h in host]
+    outs = [(torch.empty((H, W, 3)).pin_memory(), torch.empty((H, W), dtype=torch.uint8).pin_memory(),
+             torch.empty((H, W)).pin_memory()) for _ in range(S)]
+
+    def e2e_worker(s, n):
+        for _ in range(n):
+            k = pos[s] % nframes
+            streams[s].push_gray8_host(hl[s][k], hr[s][k], *outs[s])
+            pos[s] += 1
+
+    ths = [th.Thread(target=e2e_worker, args=(s, 2)) for s in range(S)]
+    [t.start() for t in ths]
+    [t.join() for t in ths]
     barrier()
     torch.cuda.synchronize()
-    for k in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        s.push_gray8_host(h_l[i % nframes], h_r[i % nframes], comp, mask, dense)
-        e2e_ms.append(1000.0 * (time.perf_counter() - t0))
-        i += 1
+    w0 = time.perf_counter()
+    ths = [th.Thread(target=e2e_worker, args=(s, args.steps)) for s in range(S)]
+    [t.start() for t in ths]
+    [t.join() for t in ths]
+    e2e_total = 1000.0 * (time.perf_counter() - w0)
     barrier()
-    e2e_total = sum(e2e_ms)
 
-    # max over ranks
     tot = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     total_ms, e2e_total = tot.tolist()
     if rank != 0:
-        s.close()
+        for st in streams:
+            st.close()
         if dist:
             dist.destroy_process_group()
         return
 
-    value = world * args.steps / (total_ms / 1000.0)
-    e2e_value = world * args.steps / (e2e_total / 1000.0)
+    frames = world * S * args.steps
+    value = frames / (total_ms / 1000.0)
+    e2e_value = frames / (e2e_total / 1000.0)
     per_frame = {k: v / max(nt, 1) for k, v in spans.items()}
     dominant = max(per_frame, key=per_frame.get)
     peak, peak_src = peaks()
@@ -325,33 +363,37 @@ def run_ours(args, world, rank, local):
             traffic = json.load(open(tp)).get(dominant)
         roof = {"kernel": dominant, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes": ab, "ms_per_launch": per_frame[dominant]}
+                "algorithmic_bytes": ab, "ms_per_launch": per_frame[dominant],
+                "timing": "CUDA events around the span, one stream alone (5 frames)"}
     agg_ab = algorithmic_bytes("aggregate", 0)
-    stages = {k: round(v, 4) for k, v in per_frame.items()}
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-        "config": {"workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+composite), "
-                               "1 stream per GPU", "width": W, "height": H, "disparities": D,
-                   "l2": "flushed between steps (256 MiB memset outside the step events)",
-                   "parallelism": "stream-sharded x%d" % world},
+        "config": {"workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+composite)",
+                   "width": W, "height": H, "disparities": D, "streams_per_gpu": S, "frames_per_step": S * world,
+                   "l2": "flushed (256 MiB memset) before every frame, inside the timed region",
+                   "parallelism": "stream-sharded x%d, %d concurrent streams per GPU" % (world, S)},
         "roofline": roof,
         "aggregation_roofline": {"achieved": agg_ab / (per_frame["aggregate"] / 1000.0) / 1e9, "peak": peak,
                                  "unit": "GB/s", "frac": agg_ab / (per_frame["aggregate"] / 1000.0) / 1e9 / peak},
-        "stage_ms": stages,
+        "stage_ms": {k: round(v, 4) for k, v in per_frame.items()},
+        "frame_ms_isolated": round(sum(per_frame.values()), 4),
         "densify_iterations": iters,
-        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": 2 * NF,
-                "d2h_bytes_per_step": NF * 3 * 4 + NF + NF * 4},
+        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": 2 * NF * S * world,
+                "d2h_bytes_per_step": (NF * 3 * 4 + NF + NF * 4) * S * world,
+                "path": "dco_stream_push_gray8_host (pinned host u8 in; composite, mask, dense out)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(s, dev_l, dev_r, lefts, rights, cfg, i, nframes)
+            line["cpu_baseline"] = cpu_baseline(streams[0], dev_l[0], dev_r[0], [f[0] for f in host[0]],
+                                                [f[1] for f in host[0]], cfg, pos[0], nframes)
         except Exception as e:  # report, don't hide
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
-    s.close()
+    for st in streams:
+        st.close()
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
@@ -372,7 +414,7 @@ def cpu_baseline(s, dev_l, dev_r, lefts, rights, cfg, i, nframes):
     vdepth[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = 1.5
     vrgb[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = (1.0, 0.55, 0.1)
     _VIRT = (vrgb, vdepth)
-    procs = min(os.cpu_count() or 1, 8)
+    procs = cpu_procs()
     # previous dense of the frame before each sampled frame (from the GPU stream)
     d_pre = torch.empty((H, W), dtype=torch.float32, device="cuda")
     frames, pres = [], []
@@ -395,10 +437,11 @@ def cpu_baseline(s, dev_l, dev_r, lefts, rights, cfg, i, nframes):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=4, help="concurrent pipeline streams per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

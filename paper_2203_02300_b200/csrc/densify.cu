@@ -18,6 +18,8 @@
 #include <cooperative_groups.h>
 #include <math.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -999,6 +1001,21 @@ void assemble_system_dev(dco_ctx* ctx, const float* sparse, const uint8_t* edges
     launched(ctx, "k_reduce_parts");
 }
 
+// Grid-wide cooperative solves from different contexts/streams must never be
+// co-scheduled (two partially-resident persistent grids could wait on each
+// other forever): every cooperative launch in the process is chained after
+// the previous one on the device through one event.
+void launch_cooperative_serialized(dco_ctx* ctx, void* fn, dim3 grid, dim3 block, void** params, size_t smem) {
+    static std::mutex mu;
+    static cudaEvent_t done[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    cudaEvent_t& ev = done[ctx->device & 63];
+    if (!ev) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event create");
+    cuda_check(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait previous solve");
+    cuda_check(cudaLaunchCooperativeKernel(fn, grid, block, params, smem, ctx->stream), "cooperative launch");
+    cuda_check(cudaEventRecord(ev, ctx->stream), "record solve");
+}
+
 // The whole PCG+MR solve, one cooperative launch. Scalars (anchors, constant
 // term) may live on the device. out_dev receives SolveOut.
 void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
@@ -1073,16 +1090,13 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
         cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
         void* params[] = {&a, &chunk_arg, &bar};
-        cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(sms), dim3(kOnchipThreadsUsed),
-                                               params, smem, ctx->stream),
-                   "launch k_pcg_onchip");
+        launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(kOnchipThreadsUsed),
+                                      params, smem);
         launched(ctx, "k_pcg_onchip");
         return;
     }
     void* params[] = {&a};
-    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_pcg), dim3(nb), dim3(512), params, 0,
-                                           ctx->stream),
-               "launch k_pcg");
+    launch_cooperative_serialized(ctx, reinterpret_cast<void*>(k_pcg), dim3(nb), dim3(512), params, 0);
     launched(ctx, "k_pcg");
 }
 

@@ -35,6 +35,19 @@ def context(device=None):
     return ctx
 
 
+def new_context(torch_stream, device=None):
+    """A dedicated dco_ctx bound to `torch_stream` (own scratch pool), for
+    running several pipeline streams concurrently on one GPU."""
+    lib = native.load()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    h = ctypes.c_void_p()
+    st = lib.dco_create(dev, ctypes.byref(h))
+    if st != 0:
+        raise RuntimeError("dco_create failed (%d)" % st)
+    lib.dco_set_stream(h.value, ctypes.c_void_p(torch_stream.cuda_stream))
+    return h.value
+
+
 def kernel_launches(device=None):
     return native.load().dco_kernel_launches(context(device))
 
@@ -406,9 +419,10 @@ def composite(real_rgb, dense, virt_rgb, virt_depth):
 class Stream:
     """One device-resident pipeline stream (pipeline.cpp:131-258 per frame)."""
 
-    def __init__(self, full_w, full_h, cfg: Config):
+    def __init__(self, full_w, full_h, cfg: Config, ctx=None):
         self.lib = native.load()
-        self.ctx = context()
+        self.own_ctx = ctx is not None
+        self.ctx = ctx if ctx is not None else context()
         h = ctypes.c_void_p()
         native.check(self.ctx, self.lib.dco_stream_create(self.ctx, full_w, full_h, ctypes.byref(cfg), ctypes.byref(h)))
         self.handle = h.value
@@ -425,19 +439,26 @@ class Stream:
         except Exception:
             pass
 
+    def _bind(self):
+        if not self.own_ctx:
+            context()
+
+    def launches(self):
+        return self.lib.dco_kernel_launches(self.ctx)
+
     def set_virtual(self, virt_rgb, virt_depth):
-        context()
+        self._bind()
         native.check(self.ctx, self.lib.dco_stream_set_virtual(self.handle, _p(virt_rgb), _p(virt_depth)))
 
     def push_gray8(self, left8, right8, rgb8=None, want_result=True):
-        context()
+        self._bind()
         res = native.FrameResult()
         native.check(self.ctx, self.lib.dco_stream_push_gray8(
             self.handle, _p(left8), _p(right8), _p(rgb8), ctypes.byref(res) if want_result else None))
         return res if want_result else None
 
     def push_f32(self, left, right, rgb=None, want_result=True):
-        context()
+        self._bind()
         res = native.FrameResult()
         native.check(self.ctx, self.lib.dco_stream_push_f32(
             self.handle, _p(left), _p(right), _p(rgb), ctypes.byref(res) if want_result else None))
@@ -445,7 +466,7 @@ class Stream:
 
     def push_gray8_host(self, left8, right8, comp_out=None, mask_out=None, dense_out=None):
         """Host numpy/pinned buffers in and out (end-to-end path)."""
-        context()
+        self._bind()
         res = native.FrameResult()
 
         def hp(a):
