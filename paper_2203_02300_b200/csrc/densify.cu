@@ -641,8 +641,14 @@ struct GridBar {
 template <int K>
 __device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, double* partials, unsigned& gen,
                                                double* sm, int* sm_flag, double (&res)[K]) {
+    // Monotonic arrival counter (never reset inside a solve): barrier g is
+    // complete when count reaches nb*(g+1). Partial rows alternate between two
+    // slots, so a block one barrier ahead never overwrites rows still being
+    // read. After the barrier every block sums all rows in block order (fixed
+    // shape: identical bits everywhere), so no block sits on the release path.
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nb = gridDim.x;
+    double* slot = partials + (gen & 1u) * (static_cast<size_t>(nb) * 8);
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
@@ -652,59 +658,44 @@ __device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, dou
         for (int k = 0; k < K; ++k) sm[warp * K + k] = v[k];
     __syncthreads();
     if (warp == 0) {
-        double bs[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             double s = lane < nw ? sm[lane * K + k] : 0.0;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            bs[k] = s;
+            if (lane == 0) __stcg(slot + blockIdx.x * 8 + k, s);
         }
-        unsigned arrived = 0;
         if (lane == 0) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) __stcg(partials + blockIdx.x * 8 + k, bs[k]);
-            // release my partial row, acquire everyone's (acq_rel RMW)
-            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(&bar->count) : "memory");
+            const unsigned target = static_cast<unsigned>(nb) * (gen + 1u);
+            unsigned c;
+            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(c) : "l"(&bar->count) : "memory");
+            ++c;
+            while (c < target) asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(c) : "l"(&bar->count) : "memory");
         }
-        arrived = __shfl_sync(0xffffffffu, arrived, 0);
-        const int slot = gen & 1u;
-        if (arrived == static_cast<unsigned>(nb) - 1u) {
-            // last arrival: all rows are visible; sum them in block order
-            double acc[K];
+    }
+    __syncthreads();
+    // all rows visible: warps 0..ceil(nb/32)-1 reduce them (fixed tree)
+    double* sres = sm + 32 * K;
+    const int nwr = (nb + 31) >> 5;
+    if (warp < nwr) {
+        const int b = warp * 32 + lane;
 #pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] = 0.0;
-            for (int b = lane; b < nb; b += 32)
+        for (int k = 0; k < K; ++k) {
+            double s = b < nb ? __ldcg(slot + b * 8 + k) : 0.0;
 #pragma unroll
-                for (int k = 0; k < K; ++k) acc[k] += __ldcg(partials + b * 8 + k);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                double s = acc[k];
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-                if (lane == 0) {
-                    __stcg(&bar->result[slot][k], s);
-                    sm[k] = s;
-                }
-            }
-            if (lane == 0) {
-                bar->count = 0u;
-                asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&bar->gen), "r"(gen + 1u) : "memory");
-            }
-        } else if (lane == 0) {
-            unsigned g;
-            do {
-                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(&bar->gen) : "memory");
-            } while (g == gen);
-#pragma unroll
-            for (int k = 0; k < K; ++k) sm[k] = __ldcg(&bar->result[slot][k]);
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) sres[warp * K + k] = s;
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < K; ++k) res[k] = sm[k];
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int i = 0; i < nwr; ++i) s += sres[i * K + k];
+        res[k] = s;
+    }
     ++gen;
-    __syncthreads();  // sm reused by the next reduction
+    __syncthreads();  // sm / sres reused by the next reduction
 }
 
 template <int EPT, int THREADS>
@@ -714,7 +705,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
     // a global halo copy for the SpMV. Solver arithmetic uses explicit FMAs:
     // the solve is tolerance-matched (not bit-exact), which halves FP64 work.
     extern __shared__ double sx[];  // [4][chunk]: x, xs, rs, qz
-    __shared__ double sm[32 * 5];
+    __shared__ double sm[2 * 32 * 5];
     __shared__ int sm_flag;
     const int w = a.w, h = a.h;
     const int n = static_cast<int>(a.n);
@@ -733,7 +724,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
     const double* __restrict__ cv = a.cv + base + t;
     double* pg = a.p + base + t;
     const double* __restrict__ prec = a.prec + base + t;
-    unsigned gen = *reinterpret_cast<volatile unsigned*>(&bar->gen);
+    unsigned gen = 0;  // barriers completed in this solve (bar->count was zeroed at launch)
     double r[EPT], p[EPT];
     uint64_t nbr = 0;  // 4 bits per slot (EPT <= 16): 1 right, 2 left, 4 down, 8 up
 #define DCO_OK(k) ((k) < nv)

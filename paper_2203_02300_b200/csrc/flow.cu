@@ -141,13 +141,19 @@ __global__ void __launch_bounds__(kPatchThreads) k_flow_patch(const float* __res
     double mse = 0.0;
     const float fw = static_cast<float>(w), fh = static_cast<float>(h);
     for (int iter = 0; iter < kIters; ++iter) {
-        double bu = 0.0, bv = 0.0, sse = 0.0;
-#pragma unroll 16
+        // all 64 residuals first (independent samples: full ILP), then the
+        // three sums in the reference's sequential (dy, dx) order
+        float rr[kPatch * kPatch];
+#pragma unroll
         for (int n = 0; n < kPatch * kPatch; ++n) {
-            int dy = n >> 3, dx = n & 7;
-            float sx = static_cast<float>(px + dx) + u;
-            float sy = static_cast<float>(py + dy) + v;
-            float r = sample_bilinear(to, w, h, sx, sy) - s_t[n * kPatchThreads + tid];
+            float sx = static_cast<float>(px + (n & 7)) + u;
+            float sy = static_cast<float>(py + (n >> 3)) + v;
+            rr[n] = sample_bilinear(to, w, h, sx, sy) - s_t[n * kPatchThreads + tid];
+        }
+        double bu = 0.0, bv = 0.0, sse = 0.0;
+#pragma unroll
+        for (int n = 0; n < kPatch * kPatch; ++n) {
+            float r = rr[n];
             bu += static_cast<double>(s_gx[n * kPatchThreads + tid]) * r;
             bv += static_cast<double>(s_gy[n * kPatchThreads + tid]) * r;
             sse += static_cast<double>(r) * r;

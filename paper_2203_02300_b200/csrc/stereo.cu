@@ -531,6 +531,385 @@ __global__ void __launch_bounds__(256) k_hist_refine(const float* __restrict__ c
 }
 
 
+// Thread per pixel: a private 16-bit histogram column per thread in shared
+// memory ([bin][thread], conflict-free), filled by walking the cross region
+// row by row (counts are integers: any order is exact), then the reference's
+// ascending mode scan over the touched bin range, which is cleared for the
+// next pixel. Used when the bin range fits (<= 256 bins); otherwise the
+// warp-per-pixel kernel above.
+constexpr int kHistThreads = 128;
+
+__global__ void __launch_bounds__(kHistThreads) k_hist_refine_thread(
+    const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ L, const uint8_t* __restrict__ R,
+    const uint8_t* __restrict__ U, const uint8_t* __restrict__ D, const int* __restrict__ bin_max_ptr, int nbins_cap,
+    float* __restrict__ next) {
+    extern __shared__ unsigned short hcol[];  // [nbins_cap][kHistThreads]
+    const int t = threadIdx.x;
+    const int bin_max = *bin_max_ptr;
+    const int nb = min(bin_max + 1, nbins_cap);
+    for (int b = 0; b < nb; ++b) hcol[b * kHistThreads + t] = 0;
+    const size_t npix = static_cast<size_t>(w) * h;
+    for (size_t p = static_cast<size_t>(blockIdx.x) * kHistThreads + t; p < npix;
+         p += static_cast<size_t>(gridDim.x) * kHistThreads) {
+        const float center = cur[p];
+        if (!isfinite(center)) {
+            next[p] = center;  // removed outliers stay removed
+            continue;
+        }
+        const int x = static_cast<int>(p % w), y = static_cast<int>(p / w);
+        const int y0 = y - U[p], y1 = y + D[p];
+        int count = 0, lo = bin_max, hi = 0;
+        for (int vy = y0; vy <= y1; ++vy) {
+            const size_t vi = static_cast<size_t>(vy) * w + x;
+            const float* row = cur + static_cast<size_t>(vy) * w;
+            const int x1 = x + R[vi];
+            for (int c = x - L[vi]; c <= x1; ++c) {
+                float v = row[c];
+                if (!isfinite(v)) continue;
+                int bin = min(max(static_cast<int>(lroundf(v)), 0), nb - 1);
+                unsigned short* cell = &hcol[bin * kHistThreads + t];
+                *cell = static_cast<unsigned short>(*cell + 1);
+                ++count;
+                lo = min(lo, bin);
+                hi = max(hi, bin);
+            }
+        }
+        int best_c = 0, best_b = lo;
+        for (int b = lo; b <= hi; ++b) {
+            int cnt = hcol[b * kHistThreads + t];
+            hcol[b * kHistThreads + t] = 0;
+            if (cnt > best_c) {
+                best_c = cnt;
+                best_b = b;
+            }
+        }
+        next[p] = (best_c == 1 && count >= 4) ? __int_as_float(0x7fc00000) : static_cast<float>(best_b);
+    }
+}
+
+// Histogram refinement as an exact integer cross-aggregation (the region
+// histogram of stereo.cpp:252-297 is the cross-region sum of one-hot bins):
+//   H(x, y', v) = #{c in the horizontal span of (x, y') : bin(c, y') == v}
+//   count(x, y, v) = sum over y' on the vertical arm of (x, y) of H(x, y', v)
+// Counts are integers, so any summation order is exact. Pass 1 builds per-row
+// bitmasks (one per bin) and popcounts each span; pass 2 walks each column
+// with a prefix ring and takes the mode (max count, smallest bin on ties)
+// with warp shuffles. Cost O(N * bins) instead of O(N * region) — regions
+// reach 35x35 on smooth texture.
+__global__ void k_refine_hcount(const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ L,
+                                const uint8_t* __restrict__ R, int nbp /* padded bins */,
+                                uint8_t* __restrict__ hcnt /* [y][x][nbp] */) {
+    extern __shared__ unsigned masks[];  // [nbp][words]
+    const int y = blockIdx.x;
+    const int words = (w + 31) >> 5;
+    for (int i = threadIdx.x; i < nbp * words; i += blockDim.x) masks[i] = 0u;
+    __syncthreads();
+    const float* row = cur + static_cast<size_t>(y) * w;
+    for (int x = threadIdx.x; x < w; x += blockDim.x) {
+        float v = row[x];
+        if (isfinite(v)) {
+            int b = min(max(static_cast<int>(lroundf(v)), 0), nbp - 1);
+            atomicOr(&masks[b * words + (x >> 5)], 1u << (x & 31));
+        }
+    }
+    __syncthreads();
+    const uint8_t* Lr = L + static_cast<size_t>(y) * w;
+    const uint8_t* Rr = R + static_cast<size_t>(y) * w;
+    uint8_t* out = hcnt + static_cast<size_t>(y) * w * nbp;
+    for (int e = threadIdx.x; e < w * nbp; e += blockDim.x) {
+        const int x = e / nbp, b = e - x * nbp;
+        const int a = x - Lr[x], z = x + Rr[x];  // inclusive span [a, z]
+        const unsigned* m = masks + b * words;
+        int cnt = 0;
+        for (int wd = a >> 5; wd <= (z >> 5); ++wd) {
+            unsigned bits = m[wd];
+            int lo = max(a - (wd << 5), 0), hi = min(z - (wd << 5), 31);
+            unsigned sel = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+            cnt += __popc(bits & sel);
+        }
+        out[e] = static_cast<uint8_t>(cnt);
+    }
+}
+
+template <int VPL>  // bins per lane (nbp = 32 * VPL)
+__global__ void k_refine_vmode(const float* __restrict__ cur, const uint8_t* __restrict__ hcnt, int w, int h,
+                               const uint8_t* __restrict__ U, const uint8_t* __restrict__ D, int lag, int ring_mask,
+                               float* __restrict__ next) {
+    extern __shared__ unsigned short rings[];  // per warp: [ring][32 lanes][VPL]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int x = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (x >= w) return;
+    const int nbp = 32 * VPL;
+    const int ring = ring_mask + 1;
+    unsigned short* rg = rings + static_cast<size_t>(warp) * ring * 32 * VPL;
+    auto R_at = [&](int slot, int j) -> unsigned short& { return rg[(slot * 32 + lane) * VPL + j]; };
+    unsigned short C[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+        C[j] = 0;
+        R_at(0, j) = 0;
+    }
+    auto finalize = [&](int py) {
+        const size_t i = static_cast<size_t>(py) * w + x;
+        const float center = cur[i];
+        const int a = py - U[i], b = py + D[i] + 1;
+        int best_c = 0, best_b = 0x7fffffff, total = 0;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            int cnt = static_cast<int>(R_at(b & ring_mask, j)) - static_cast<int>(R_at(a & ring_mask, j));
+            int bin = lane * VPL + j;
+            total += cnt;
+            if (cnt > best_c) {  // ascending bins within the lane: first max kept
+                best_c = cnt;
+                best_b = bin;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            total += __shfl_xor_sync(0xffffffffu, total, off);
+            int oc = __shfl_xor_sync(0xffffffffu, best_c, off);
+            int ob = __shfl_xor_sync(0xffffffffu, best_b, off);
+            if (oc > best_c || (oc == best_c && ob < best_b)) {
+                best_c = oc;
+                best_b = ob;
+            }
+        }
+        if (lane == 0) {
+            float o = center;  // removed outliers stay removed
+            if (isfinite(center))
+                o = (best_c == 1 && total >= 4) ? __int_as_float(0x7fc00000) : static_cast<float>(best_b);
+            next[i] = o;
+        }
+    };
+    const size_t rowstride = static_cast<size_t>(w) * nbp;
+    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
+    for (int y = 0; y < h; ++y) {
+        const uint8_t* hp = src + y * rowstride;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            C[j] = static_cast<unsigned short>(C[j] + hp[j]);
+            R_at((y + 1) & ring_mask, j) = C[j];
+        }
+        __syncwarp();
+        const int py = y + 1 - lag;
+        if (py >= 0) finalize(py);
+        __syncwarp();
+    }
+    for (int py = max(h + 1 - lag, 0); py < h; ++py) finalize(py);
+}
+
+// Column prefix carries for the segmented mode pass: for every column x, bin
+// lane-group and segment k, the exclusive prefix sum of H over the rows
+// before j0(k) = max(0, k*seg - lag) (integers: exact in any order).
+template <int VPL>
+__global__ void k_refine_carry(const uint8_t* __restrict__ hcnt, int w, int h, int seg, int nseg, int lag,
+                               unsigned* __restrict__ carry /* [x][nseg][32 lanes] packed u16 x VPL in u32s */) {
+    const int lane = threadIdx.x & 31;
+    const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (x >= w) return;
+    const int nbp = 32 * VPL;
+    const size_t rowstride = static_cast<size_t>(w) * nbp;
+    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
+    unsigned acc[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) acc[j] = 0;
+    int y = 0;
+    for (int k = 0; k < nseg; ++k) {
+        const int j0 = max(0, k * seg - lag);
+        for (; y < j0; ++y) {
+            const uint8_t* hp = src + y * rowstride;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) acc[j] += hp[j];
+        }
+        unsigned* dst = carry + ((static_cast<size_t>(x) * nseg + k) * 32 + lane) * VPL;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) dst[j] = acc[j];
+    }
+}
+
+// Segmented mode pass: warp per (column x, row segment k); the prefix ring is
+// seeded from the carry, so segments run in parallel. H rows are prefetched
+// kPF ahead.
+template <int VPL>
+__global__ void k_refine_vmode2(const float* __restrict__ cur, const uint8_t* __restrict__ hcnt, int w, int h,
+                                const uint8_t* __restrict__ U, const uint8_t* __restrict__ D, int lag, int ring_mask,
+                                int seg, int nseg, const unsigned* __restrict__ carry, float* __restrict__ next) {
+    extern __shared__ unsigned short rings[];  // per warp: [ring][32 lanes][VPL]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+    const int x = gw / nseg, k = gw - x * nseg;
+    if (x >= w) return;
+    const int nbp = 32 * VPL;
+    const int ring = ring_mask + 1;
+    unsigned short* rg = rings + static_cast<size_t>(warp) * ring * 32 * VPL;
+    auto R_at = [&](int slot, int j) -> unsigned short& { return rg[(slot * 32 + lane) * VPL + j]; };
+    const int j0 = max(0, k * seg - lag);
+    const int out0 = k * seg, out1 = min(h, (k + 1) * seg);
+    const int yend = min(h, out1 + lag);  // rows needed: C up to out1 - 1 + maxarm + 1
+    unsigned short C[VPL];
+    unsigned cs[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) cs[j] = 0;
+    for (int kk = 0; kk < k; ++kk) {  // exclusive prefix of the segment sums
+        const unsigned* cin = carry + ((static_cast<size_t>(x) * nseg + kk) * 32 + lane) * VPL;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) cs[j] += cin[j];
+    }
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+        C[j] = static_cast<unsigned short>(cs[j]);
+        R_at(j0 & ring_mask, j) = C[j];
+    }
+    auto finalize = [&](int py, float center, int up, int dn) {
+        const size_t i = static_cast<size_t>(py) * w + x;
+        const int a = py - up, b = py + dn + 1;
+        int best_c = 0, best_b = 0x7fffffff, total = 0;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+            int cnt = static_cast<int>(R_at(b & ring_mask, j)) - static_cast<int>(R_at(a & ring_mask, j));
+            total += cnt;
+            if (cnt > best_c) {
+                best_c = cnt;
+                best_b = lane * VPL + j;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            total += __shfl_xor_sync(0xffffffffu, total, off);
+            int oc = __shfl_xor_sync(0xffffffffu, best_c, off);
+            int ob = __shfl_xor_sync(0xffffffffu, best_b, off);
+            if (oc > best_c || (oc == best_c && ob < best_b)) {
+                best_c = oc;
+                best_b = ob;
+            }
+        }
+        if (lane == 0) {
+            float o = center;
+            if (isfinite(center))
+                o = (best_c == 1 && total >= 4) ? __int_as_float(0x7fc00000) : static_cast<float>(best_b);
+            next[i] = o;
+        }
+    };
+    const size_t rowstride = static_cast<size_t>(w) * nbp;
+    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
+    constexpr int kPF = 8;
+    uint8_t pf[kPF][VPL];
+#pragma unroll
+    for (int q = 0; q < kPF; ++q)
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) pf[q][j] = (j0 + q < yend) ? src[(j0 + q) * rowstride + j] : 0;
+    for (int y0 = j0; y0 < yend; y0 += kPF) {
+        uint8_t nx[kPF][VPL];
+#pragma unroll
+        for (int q = 0; q < kPF; ++q)
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) {
+                int y = y0 + kPF + q;
+                nx[q][j] = y < yend ? src[y * rowstride + j] : 0;
+            }
+        // the centre values / vertical arms of the rows finalised in this chunk
+        float cq[kPF];
+        int uq[kPF], dq[kPF];
+#pragma unroll
+        for (int q = 0; q < kPF; ++q) {
+            const int py = y0 + q + 1 - lag;
+            cq[q] = 0.0f;
+            uq[q] = dq[q] = 0;
+            if (py >= out0 && py < out1) {
+                const size_t i = static_cast<size_t>(py) * w + x;
+                cq[q] = cur[i];
+                uq[q] = U[i];
+                dq[q] = D[i];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kPF; ++q) {
+            const int y = y0 + q;
+            if (y < yend) {
+#pragma unroll
+                for (int j = 0; j < VPL; ++j) {
+                    C[j] = static_cast<unsigned short>(C[j] + pf[q][j]);
+                    R_at((y + 1) & ring_mask, j) = C[j];
+                }
+                const int py = y + 1 - lag;
+                if (py >= out0 && py < out1) finalize(py, cq[q], uq[q], dq[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kPF; ++q)
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) pf[q][j] = nx[q][j];
+    }
+    // rows whose window reaches the image bottom
+    for (int py = max(yend + 1 - lag, out0); py < out1; ++py) {
+        const size_t i = static_cast<size_t>(py) * w + x;
+        finalize(py, cur[i], U[i], D[i]);
+    }
+}
+
+// H(x, y, .) by scattering the pixel's own span (<= 2*l1+1 values) into a
+// per-thread shared-memory column of u8 counters, then streaming the dense
+// row out with 16-byte stores (the zero bins included).
+constexpr int kHcThreads = 128;
+__global__ void __launch_bounds__(kHcThreads) k_refine_hscatter(const float* __restrict__ cur, int w, int h,
+                                                                const uint8_t* __restrict__ L,
+                                                                const uint8_t* __restrict__ R, int nbp,
+                                                                uint8_t* __restrict__ hcnt) {
+    extern __shared__ uint4 hsm4[];  // [nbp/16][kHcThreads] uint4
+    uint8_t* hs = reinterpret_cast<uint8_t*>(hsm4);
+    const int t = threadIdx.x;
+    const int nq = nbp >> 4;
+    for (int q = 0; q < nq; ++q) hsm4[q * kHcThreads + t] = make_uint4(0, 0, 0, 0);
+    const size_t npix = static_cast<size_t>(w) * h;
+    for (size_t p = static_cast<size_t>(blockIdx.x) * kHcThreads + t; p < npix;
+         p += static_cast<size_t>(gridDim.x) * kHcThreads) {
+        const int x = static_cast<int>(p % w);
+        const float* row = cur + (p - x);
+        const int a = x - L[p], z = x + R[p];
+        int lo = nbp, hi = -1;
+        for (int c = a; c <= z; ++c) {
+            float v = row[c];
+            if (!isfinite(v)) continue;
+            int b = min(max(static_cast<int>(lroundf(v)), 0), nbp - 1);
+            uint8_t* cell = &hs[((b >> 4) * kHcThreads + t) * 16 + (b & 15)];
+            *cell = static_cast<uint8_t>(*cell + 1);
+            lo = min(lo, b);
+            hi = max(hi, b);
+        }
+        uint4* out = reinterpret_cast<uint4*>(hcnt + p * nbp);
+        for (int q = 0; q < nq; ++q) {
+            uint4 val = hsm4[q * kHcThreads + t];
+            out[q] = val;
+        }
+        for (int q = (lo >> 4); q <= (hi >> 4) && hi >= 0; ++q) hsm4[q * kHcThreads + t] = make_uint4(0, 0, 0, 0);
+    }
+}
+
+// Per (column, segment) sums of H over the rows [j0(k), j0(k+1)); the mode
+// pass turns them into exclusive prefixes (integers: exact in any order).
+template <int VPL>
+__global__ void k_refine_segsum(const uint8_t* __restrict__ hcnt, int w, int h, int seg, int nseg, int lag,
+                                unsigned* __restrict__ segsum /* [x][nseg][32][VPL] */) {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int x = gw / nseg, k = gw - x * nseg;
+    if (x >= w) return;
+    const int nbp = 32 * VPL;
+    const int y0 = max(0, k * seg - lag), y1 = (k + 1 < nseg) ? max(0, (k + 1) * seg - lag) : h;
+    const size_t rowstride = static_cast<size_t>(w) * nbp;
+    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
+    unsigned acc[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) acc[j] = 0;
+#pragma unroll 8
+    for (int y = y0; y < y1; ++y)
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) acc[j] += src[y * rowstride + j];
+    unsigned* dst = segsum + ((static_cast<size_t>(x) * nseg + k) * 32 + lane) * VPL;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) dst[j] = acc[j];
+}
+
 // -------------------------------------------------------- sparse depth -----
 // disparity_to_sparse_depth, stereo.cpp:301-315.
 __global__ void k_sparse_depth(const float* __restrict__ disp, int w, int h, double fb, int fw,
@@ -728,10 +1107,72 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
                       static_cast<float*>(scratch(ctx, S_DISP1, n * 4))};
     const float* src = disp;
     const unsigned blocks = static_cast<unsigned>(std::min<size_t>(blocks_for(n, warps), 148 * 16));
+    // exact integer cross-aggregation of one-hot bins (preferred, O(N*bins))
+    const int nbp = cap <= 32 ? 32 : cap <= 64 ? 64 : cap <= 128 ? 128 : cap <= 256 ? 256 : 0;
+    uint8_t* hcnt = nbp ? static_cast<uint8_t*>(scratch(ctx, S_HSUM, n * nbp)) : nullptr;
+    const int lag = max_arm + 1, ring = ring_size(max_arm);
+    const int vwarps = 4;
+    const size_t vsmem = static_cast<size_t>(vwarps) * ring * nbp * sizeof(unsigned short);
+    const size_t hsmem = static_cast<size_t>(nbp) * ((w + 31) / 32) * sizeof(unsigned);
+    static bool attr_v = false;
+    if (!attr_v) {
+        cudaFuncSetAttribute(k_refine_hcount, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_v = true;
+    }
+    const bool aggregated = nbp && vsmem <= 200 * 1024 && hsmem <= 200 * 1024;
+    const bool per_thread = cap <= 256;
+    const size_t smem_t = static_cast<size_t>(cap) * kHistThreads * sizeof(unsigned short);
+    static bool attr_t = false;
+    if (per_thread && !attr_t) {
+        cudaFuncSetAttribute(k_hist_refine_thread, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_t = true;
+    }
+    const unsigned blocks_t = static_cast<unsigned>(std::min<size_t>(blocks_for(n, kHistThreads), 148 * 8));
     for (int it = 0; it < iters; ++it) {
         float* dst = (it == iters - 1) ? out : bufs[it & 1];
-        k_hist_refine<<<blocks, warps * 32, smem, ctx->stream>>>(src, w, h, l, r, u, d, bmax, cap, rows_cap, dst);
-        launched(ctx, "k_hist_refine");
+        if (aggregated) {
+            k_refine_hscatter<<<static_cast<unsigned>(std::min<size_t>(blocks_for(n, kHcThreads), 148 * 8)),
+                                kHcThreads, static_cast<size_t>(nbp) * kHcThreads, ctx->stream>>>(src, w, h, l, r,
+                                                                                                  nbp, hcnt);
+            launched(ctx, "k_refine_hscatter");
+            const int seg = 32, nseg = (h + seg - 1) / seg;
+            unsigned* carry = static_cast<unsigned*>(scratch(ctx, S_TMP1, static_cast<size_t>(w) * nseg * nbp * 4));
+            dim3 vb(32 * vwarps), vg((w * nseg + vwarps - 1) / vwarps);
+            switch (nbp / 32) {
+                case 1:
+                    k_refine_segsum<1><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                    k_refine_vmode2<1><<<vg, vb, vsmem, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring - 1, seg, nseg, carry, dst);
+                    break;
+                case 2:
+                    k_refine_segsum<2><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                    k_refine_vmode2<2><<<vg, vb, vsmem, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring - 1, seg, nseg, carry, dst);
+                    break;
+                case 4:
+                    k_refine_segsum<4><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                    k_refine_vmode2<4><<<vg, vb, vsmem, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring - 1, seg, nseg, carry, dst);
+                    break;
+                default:
+                    k_refine_segsum<8><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                    k_refine_vmode2<8><<<vg, vb, vsmem, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring - 1, seg, nseg, carry, dst);
+                    break;
+            }
+            launched(ctx, "k_refine_carry");
+            launched(ctx, "k_refine_vmode");
+        } else if (per_thread) {
+            k_hist_refine_thread<<<blocks_t, kHistThreads, smem_t, ctx->stream>>>(src, w, h, l, r, u, d, bmax, cap, dst);
+            launched(ctx, "k_hist_refine_thread");
+        } else {
+            k_hist_refine<<<blocks, warps * 32, smem, ctx->stream>>>(src, w, h, l, r, u, d, bmax, cap, rows_cap, dst);
+            launched(ctx, "k_hist_refine");
+        }
         src = dst;
     }
 }

@@ -32,3 +32,6 @@ for tag, m in (("block0", a), ("last", b)):
     print(tag, "cycles/iter %.0f" % tot)
     for n, v in zip(names, d):
         print("   %-16s %8.0f" % (n, v))
+    e = m[5:40]
+    print("   B: work-end->arrive %.0f  atomic %.0f  arrive->released %.0f  released->B-end %.0f" % (
+        (e[:, 7] - e[:, 3]).mean(), (e[:, 8] - e[:, 7]).mean(), (e[:, 9] - e[:, 8]).mean(), (e[:, 4] - e[:, 9]).mean()))
