@@ -21,6 +21,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "grid_reduce.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -566,167 +567,52 @@ __global__ void __launch_bounds__(512) k_pcg(CGArgs a) {
 }
 
 // ------------------------------------------------- on-chip resident solver --
-// Same algorithm and reductions as k_pcg, but each of the grid's blocks (one
-// per SM, 1024 threads) owns a contiguous chunk of unknowns for the whole
-// solve: r and p live in registers (EPT per thread), x / xs / rs and the
-// q-then-z scratch live in shared memory. Only p crosses blocks (written to
-// a global halo array once per iteration for the SpMV); the coefficient
-// arrays and the Jacobi preconditioner stream from L2. Per iteration: 3 grid
-// barriers (SpMV halo + 2 reductions; the |rs|^2 reduction shares the halo
-// barrier). Block reductions finish in warp 0 (one CTA barrier each).
-constexpr int kOnchipThreads = 1024;
-
-// per-thread partials -> this block's partial row in global memory
-template <int K>
-__device__ __forceinline__ void block_partial(double (&v)[K], double* sm_part, double* out) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
-    if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < K; ++k) sm_part[warp * K + k] = v[k];
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double t = lane < nw ? sm_part[lane * K + k] : 0.0;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-            if (lane == 0) out[k] = t;
-        }
-    }
-}
-
-// all blocks' partial rows -> totals, identical (same order) in every block:
-// warp i loads partials [32i, 32i+32) and tree-reduces them, then every
-// thread adds the per-warp sums in warp order.
-template <int K>
-__device__ __forceinline__ void grid_reduce(const double* part, int stride, int nb, double (&res)[K],
-                                            double* sm_res /* [32*K] */) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nw = (nb + 31) >> 5;
-    if (warp < nw) {
-        const int b = warp * 32 + lane;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double s = b < nb ? part[b * stride + k] : 0.0;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            if (lane == 0) sm_res[warp * K + k] = s;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double s = 0.0;
-        for (int i = 0; i < nw; ++i) s += sm_res[i * K + k];
-        res[k] = s;
-    }
-}
-
-// Grid-wide deterministic all-reduce fused with the grid barrier: every block
-// publishes its partial row and arrives on a counter; the LAST block to
-// arrive sums all rows in block order (fixed, so every run and every block
-// sees identical bits), publishes the totals and releases the others. One
-// barrier instead of "grid.sync + every block re-reading every partial".
-struct GridBar {
-    unsigned count;
-    unsigned gen;
-    unsigned pad[30];
-    double result[2][8];
-};
-
-template <int K>
-__device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, double* partials, unsigned& gen,
-                                               double* sm, int* sm_flag, double (&res)[K]) {
-    // Monotonic arrival counter (never reset inside a solve): barrier g is
-    // complete when count reaches nb*(g+1). Partial rows alternate between two
-    // slots, so a block one barrier ahead never overwrites rows still being
-    // read. After the barrier every block sums all rows in block order (fixed
-    // shape: identical bits everywhere), so no block sits on the release path.
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int nb = gridDim.x;
-    double* slot = partials + (gen & 1u) * (static_cast<size_t>(nb) * 8);
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
-    if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < K; ++k) sm[warp * K + k] = v[k];
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double s = lane < nw ? sm[lane * K + k] : 0.0;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            if (lane == 0) __stcg(slot + blockIdx.x * 8 + k, s);
-        }
-        if (lane == 0) {
-            const unsigned target = static_cast<unsigned>(nb) * (gen + 1u);
-            unsigned c;
-            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(c) : "l"(&bar->count) : "memory");
-            ++c;
-            while (c < target) asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(c) : "l"(&bar->count) : "memory");
-        }
-    }
-    __syncthreads();
-    // all rows visible: warps 0..ceil(nb/32)-1 reduce them (fixed tree)
-    double* sres = sm + 32 * K;
-    const int nwr = (nb + 31) >> 5;
-    if (warp < nwr) {
-        const int b = warp * 32 + lane;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double s = b < nb ? __ldcg(slot + b * 8 + k) : 0.0;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            if (lane == 0) sres[warp * K + k] = s;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double s = 0.0;
-        for (int i = 0; i < nwr; ++i) s += sres[i * K + k];
-        res[k] = s;
-    }
-    ++gen;
-    __syncthreads();  // sm / sres reused by the next reduction
-}
-
+// Same Krylov iterates as k_pcg, but each of the grid's blocks (one per SM,
+// 1024 threads) owns a contiguous chunk of unknowns for the whole solve: r and
+// x in registers (EPT per thread), p / xs / rs / q in shared memory. Only a
+// one-row halo crosses blocks per iteration; the coefficient arrays and the
+// Jacobi preconditioner stream from L2. One grid barrier + deterministic
+// all-reduce per iteration (grid_reduce.cuh).
 template <int EPT, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, GridBar* bar) {
-    // Block b owns [base, base + size): sizes differ by at most one. r and p
-    // in registers, x / xs / rs / (q then z) in shared memory, p published to
-    // a global halo copy for the SpMV. Solver arithmetic uses explicit FMAs:
-    // the solve is tolerance-matched (not bit-exact), which halves FP64 work.
-    extern __shared__ double sx[];  // [4][chunk]: x, xs, rs, qz
-    __shared__ double sm[2 * 32 * 5];
-    __shared__ int sm_flag;
+    // Block b owns [base, base + size): sizes differ by at most one. r and x
+    // in registers; p (with a one-row halo either side), xs, rs, q in shared
+    // memory. One grid barrier per iteration: every scalar of iteration k
+    // (pq, rho_{k+1}, sd, dd) is a polynomial in alpha_k of sums that are
+    // known once q_k = A p_k is, so they ride on one reduction:
+    //   rho_{k+1} = S1 - 2 a S2 + a^2 S3   (S = sum prec r r, prec r q, prec q q)
+    //   sd        = T1 - a T2              (T = sum rs (r - rs), rs q)
+    //   dd        = U1 - 2 a U2 + a^2 U3   (U = sum (r-rs)^2, (r-rs) q, q q)
+    // The vector updates of iteration k then run at the head of phase k+1,
+    // together with |rs|^2 (the reported norm, one phase late). The halo of
+    // p_{k+1} is recomputed from the (r, q, p) rows the neighbouring blocks
+    // publish in phase k, with the owner's FMA sequence (same bits). Same
+    // Krylov iterates as densify.cpp:172-207 in exact arithmetic; tolerance-
+    // matched (not bit-exact) in floating point.
+    extern __shared__ double sx[];  // p [w + chunk + w], then xs, rs, q [chunk] each
+    __shared__ double sm[32 * 16];
+    __shared__ double s_w1[32 * 4];  // per-warp P1 sums
     const int w = a.w, h = a.h;
     const int n = static_cast<int>(a.n);
     const int nb = gridDim.x;
-    const int q = n / nb, rem = n - q * nb;
-    const int base = blockIdx.x * q + min(static_cast<int>(blockIdx.x), rem);
-    const int size = q + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
+    const int qn = n / nb, rem = n - qn * nb;
+    const int base = blockIdx.x * qn + min(static_cast<int>(blockIdx.x), rem);
+    const int size = qn + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
     const int t = threadIdx.x;
     const int nv = size > t ? (size - t + THREADS - 1) / THREADS : 0;  // occupied register slots
-    double* s_x = sx + t;
-    double* s_xs = sx + chunk + t;
-    double* s_rs = sx + 2 * chunk + t;
-    double* s_qz = sx + 3 * chunk + t;
+    double* s_p = sx + w + t;
+    double* s_xs = sx + 2 * w + chunk + t;
+    double* s_rs = sx + 2 * w + 2 * chunk + t;
+    double* s_q = sx + 2 * w + 3 * chunk + t;
     const double* __restrict__ diag = a.diag + base + t;
     const double* __restrict__ ch = a.ch + base + t;
     const double* __restrict__ cv = a.cv + base + t;
-    double* pg = a.p + base + t;
     const double* __restrict__ prec = a.prec + base + t;
+    // halo rows published per phase parity: (r, q, p) in (a.r, a.q, a.p) / (a.x, a.z, a.rs)
     unsigned gen = 0;  // barriers completed in this solve (bar->count was zeroed at launch)
-    double r[EPT], p[EPT];
+    double r[EPT], x[EPT];
     uint64_t nbr = 0;  // 4 bits per slot (EPT <= 16): 1 right, 2 left, 4 down, 8 up
+    unsigned pub = 0;  // bit k: slot k lies in a row other blocks read as halo
 #define DCO_OK(k) ((k) < nv)
 #define KO(k) ((k) * THREADS)
 
@@ -743,17 +629,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
     const double cterm = a.constant_term_dev ? *a.constant_term_dev : a.constant_term_host;
 
     // setup (densify.cpp:147-166): x = initial, r = b - A x, z = M r, p = z
+    // (p_0 published whole in a.xs for phase 0's halo)
     double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // b.b, r.r, r.z, x.Ax, b.x
     {
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
             r[k] = 0.0;
-            p[k] = 0.0;
+            x[k] = 0.0;
             if (DCO_OK(k)) {
                 const int i = base + t + KO(k);
                 const int xx = i % w, y = i / w;
                 nbr |= static_cast<uint64_t>((xx + 1 < w ? 1u : 0u) | (xx > 0 ? 2u : 0u) | (y + 1 < h ? 4u : 0u) |
                                              (y > 0 ? 8u : 0u)) << (4 * k);
+                if (t + KO(k) < w || t + KO(k) >= size - w) pub |= 1u << k;
                 double ax = apply_at(a.diag, a.ch, a.cv, a.init, w, h, i, xx, y);
                 double xi = a.init[i];
                 double b = a.rhs[i];
@@ -761,13 +649,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
                 double pr = d > 0.0 ? 1.0 / d : 1.0;
                 double ri = b - ax;
                 double zi = pr * ri;
-                s_x[KO(k)] = xi;
+                x[k] = xi;
                 s_xs[KO(k)] = xi;
                 s_rs[KO(k)] = ri;
+                s_p[KO(k)] = zi;
                 a.prec[i] = pr;
                 r[k] = ri;
-                p[k] = zi;
-                a.p[i] = zi;
+                a.xs[i] = zi;
                 tot[0] += b * b;
                 tot[1] += ri * ri;
                 tot[2] += ri * zi;
@@ -775,7 +663,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
                 tot[4] += b * xi;
             }
         }
-        barrier_reduce<5>(tot, bar, a.part, gen, sm, &sm_flag, tot);
+        barrier_reduce<5>(tot, bar, a.part, gen, sm, tot);
     }
     const double bnorm = sqrt(tot[0]);
     const double denom = bnorm > 0.0 ? bnorm : 1.0;
@@ -787,113 +675,188 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
     }
 
     int iter = 0;
+    double alpha = 0.0, beta = 0.0, eta = 0.0;  // iteration iter-1's scalars, applied at the head of phase iter
 #define STAMP(j)                                                                                      \
-    if (a.dbg && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && t == 0 && iter < 64) \
-        a.dbg[(blockIdx.x ? 640 : 0) + iter * 10 + (j)] = clock64();
-    while (iter < a.max_iter && snorm / denom > a.tol) {
-        STAMP(0)
-        // A: q = A p (halo p from global), pq -- stencil order of densify.cpp:125-129
-        double pq;
-        {
-            double v[1] = {0.0};
+    if (a.dbg && t == 0 && iter < 64) {                                                               \
+        if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)                                           \
+            a.dbg[(blockIdx.x ? 640 : 0) + iter * 10 + (j)] = clock64();                              \
+        if ((j) < 3) {                                                                                \
+            unsigned long long gt;                                                                    \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));                                   \
+            a.dbg[1280 + (iter * 1024 + blockIdx.x) * 3 + (j)] = static_cast<long long>(gt);          \
+        }                                                                                             \
+    }
+    if (a.max_iter > 0 && snorm / denom > a.tol) {
+        for (;;) {
+            STAMP(0)
+            // opaque per iteration: keeps the compiler from hoisting (and
+            // spilling) per-slot bit tests out of the loop
+            asm volatile("" : "+r"(pub), "+l"(nbr));
+            const int par = iter & 1;
+            double* const hr_in = par ? a.r : a.x;  // published in phase iter-1
+            double* const hq_in = par ? a.q : a.z;
+            double* const hp_in = par ? a.p : a.rs;
+            double* const hr_out = par ? a.x : a.r;
+            double* const hq_out = par ? a.z : a.q;
+            double* const hp_out = par ? a.rs : a.p;
+            // halo rows [-w, 0) and [size, size + w): p_iter of the neighbours,
+            // recomputed with the owner's FMA sequence
+            {
+                constexpr int kHalo = 3;
+                double h0[kHalo], h1[kHalo], h2[kHalo], h3[kHalo];
+#pragma unroll
+                for (int u = 0; u < kHalo; ++u) {
+                    const int e = t + u * THREADS;
+                    const int j = base + (e < w ? e - w : size + (e - w));
+                    h0[u] = h1[u] = h2[u] = h3[u] = 0.0;
+                    if (e < 2 * w && j >= 0 && j < n) {
+                        if (iter) {
+                            h0[u] = __ldcg(hr_in + j);
+                            h1[u] = __ldcg(hq_in + j);
+                            h2[u] = __ldcg(hp_in + j);
+                            h3[u] = __ldg(a.prec + j);
+                        } else {
+                            h2[u] = __ldcg(a.xs + j);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kHalo; ++u) {
+                    const int e = t + u * THREADS;
+                    const int l = e < w ? e - w : size + (e - w);
+                    const int j = base + l;
+                    if (e < 2 * w && j >= 0 && j < n)
+                        sx[w + l] = iter ? __fma_rn(beta, h2[u], h3[u] * __fma_rn(-alpha, h1[u], h0[u])) : h2[u];
+                }
+                for (int e = t + kHalo * THREADS; e < 2 * w; e += THREADS) {  // w > 1.5 * THREADS only
+                    const int l = e < w ? e - w : size + (e - w);
+                    const int j = base + l;
+                    if (j >= 0 && j < n) {
+                        double pj;
+                        if (iter) {
+                            const double rj = __fma_rn(-alpha, __ldcg(hq_in + j), __ldcg(hr_in + j));
+                            pj = __fma_rn(beta, __ldcg(hp_in + j), __ldg(a.prec + j) * rj);
+                        } else {
+                            pj = __ldcg(a.xs + j);
+                        }
+                        sx[w + l] = pj;
+                    }
+                }
+            }
+            // P1: vector updates of iteration iter-1 (densify.cpp:178-201), then
+            // sums over the updated r / rs: |rs|^2, S1, T1, U1; publish (r, p) rows
+            double v[10];
+#pragma unroll
+            for (int c = 0; c < 10; ++c) v[c] = 0.0;
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) {
+                if (DCO_OK(k)) {
+                    const int o = KO(k);
+                    double pk = s_p[o];
+                    double ri = r[k];
+                    double rsi = s_rs[o];
+                    const double pr = prec[o];
+                    if (iter) {
+                        x[k] = __fma_rn(alpha, pk, x[k]);
+                        ri = __fma_rn(-alpha, s_q[o], ri);
+                        pk = __fma_rn(beta, pk, pr * ri);
+                        r[k] = ri;
+                        s_p[o] = pk;
+                        if (eta > 0.0) {
+                            rsi = __fma_rn(eta, ri - rsi, rsi);
+                            s_rs[o] = rsi;
+                            double xsi = s_xs[o];
+                            s_xs[o] = __fma_rn(eta, x[k] - xsi, xsi);
+                        }
+                    }
+                    const double e = ri - rsi;
+                    v[1] = __fma_rn(rsi, rsi, v[1]);
+                    v[2] = __fma_rn(pr * ri, ri, v[2]);
+                    v[3] = __fma_rn(rsi, e, v[3]);
+                    v[4] = __fma_rn(e, e, v[4]);
+                    if (pub & (1u << k)) {  // rows other blocks read as halo
+                        __stcg(hr_out + base + t + o, ri);
+                        __stcg(hp_out + base + t + o, pk);
+                    }
+                }
+            }
+            // P1 sums -> per-warp partials in shared memory (frees registers for P2)
+            {
+                const int lane = t & 31, warp = t >> 5;
+#pragma unroll
+                for (int c = 1; c <= 4; ++c) {
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], off);
+                    if (lane == 0) s_w1[warp * 4 + (c - 1)] = v[c];
+                    v[c] = 0.0;
+                }
+            }
+            __syncthreads();
+            // P2: q = A p -- stencil order of densify.cpp:125-129; pq, S2, S3, T2, U2, U3
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 if (DCO_OK(k)) {
                     const unsigned m = static_cast<unsigned>(nbr >> (4 * k));
                     const int o = KO(k);
-                    double acc = diag[o] * p[k];
-                    if (m & 1u) acc = __fma_rn(-ch[o], __ldcg(pg + o + 1), acc);
-                    if (m & 2u) acc = __fma_rn(-ch[o - 1], __ldcg(pg + o - 1), acc);
-                    if (m & 4u) acc = __fma_rn(-cv[o], __ldcg(pg + o + w), acc);
-                    if (m & 8u) acc = __fma_rn(-cv[o - w], __ldcg(pg + o - w), acc);
-                    s_qz[o] = acc;
-                    v[0] = __fma_rn(p[k], acc, v[0]);
+                    const double pk = s_p[o];
+                    double acc = diag[o] * pk;
+                    if (m & 1u) acc = __fma_rn(-ch[o], s_p[o + 1], acc);
+                    if (m & 2u) acc = __fma_rn(-ch[o - 1], s_p[o - 1], acc);
+                    if (m & 4u) acc = __fma_rn(-cv[o], s_p[o + w], acc);
+                    if (m & 8u) acc = __fma_rn(-cv[o - w], s_p[o - w], acc);
+                    s_q[o] = acc;
+                    const double ri = r[k], rsi = s_rs[o];
+                    const double pq_ = prec[o] * acc;
+                    v[0] = __fma_rn(pk, acc, v[0]);
+                    v[5] = __fma_rn(pq_, ri, v[5]);
+                    v[6] = __fma_rn(pq_, acc, v[6]);
+                    v[7] = __fma_rn(rsi, acc, v[7]);
+                    v[8] = __fma_rn(ri - rsi, acc, v[8]);
+                    v[9] = __fma_rn(acc, acc, v[9]);
+                    if (pub & (1u << k)) __stcg(hq_out + base + t + o, acc);
                 }
+            }
+            if ((t & 31) == 0) {
+#pragma unroll
+                for (int c = 1; c <= 4; ++c) v[c] = s_w1[(t >> 5) * 4 + (c - 1)];
             }
             STAMP(1)
-            double res[1];
-            barrier_reduce<1>(v, bar, a.part, gen, sm, &sm_flag, res);
-            pq = res[0];
+            double res[10];
+            barrier_reduce<10>(v, bar, a.part, gen, sm, res);
             STAMP(2)
-        }
-        if (pq <= 0.0) break;  // uniform across the grid
-        const double alpha = rho / pq;
-        // B: x, r, z; rho_next; MR numerators
-        double rho_next, sd, dd;
-        {
-            double v[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
-                if (DCO_OK(k)) {
-                    const int o = KO(k);
-                    s_x[o] = __fma_rn(alpha, p[k], s_x[o]);
-                    double ri = __fma_rn(-alpha, s_qz[o], r[k]);
-                    double zi = prec[o] * ri;
-                    r[k] = ri;
-                    s_qz[o] = zi;
-                    v[0] = __fma_rn(ri, zi, v[0]);
-                    double rsi = s_rs[o];
-                    double di = ri - rsi;
-                    v[1] = __fma_rn(rsi, di, v[1]);
-                    v[2] = __fma_rn(di, di, v[2]);
-                }
+            if (iter > 0) {
+                snorm = sqrt(res[1]);
+                if (blockIdx.x == 0 && t == 0 && iter < a.hist_cap) a.hist[iter] = snorm;
             }
-            STAMP(3)
-            double res[3];
-            barrier_reduce<3>(v, bar, a.part, gen, sm, &sm_flag, res);
-            rho_next = res[0];
-            sd = res[1];
-            dd = res[2];
-            STAMP(4)
-        }
-        const double beta = rho_next / rho;
-        rho = rho_next;
-        double eta = 0.0;
-        if (dd > 0.0) {
-            eta = -sd / dd;
-            eta = eta < 0.0 ? 0.0 : (1.0 < eta ? 1.0 : eta);
-        }
-        // C: p = z + beta p (published for the next SpMV), MR smoothing, |rs|^2
-        {
-            double v[1] = {0.0};
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
-                if (DCO_OK(k)) {
-                    const int o = KO(k);
-                    double pn = __fma_rn(beta, p[k], s_qz[o]);
-                    p[k] = pn;
-                    __stcg(pg + o, pn);
-                    double rsi = s_rs[o];
-                    if (eta > 0.0) {
-                        rsi = __fma_rn(eta, r[k] - rsi, rsi);
-                        s_rs[o] = rsi;
-                        double xsi = s_xs[o];
-                        s_xs[o] = __fma_rn(eta, s_x[o] - xsi, xsi);
-                    }
-                    v[0] = __fma_rn(rsi, rsi, v[0]);
-                }
+            if (!(iter < a.max_iter && snorm / denom > a.tol)) break;  // densify.cpp:172 (uniform)
+            const double pq = res[0];
+            if (pq <= 0.0) break;
+            alpha = rho / pq;
+            const double rho_next = __fma_rn(alpha * alpha, res[6], __fma_rn(-2.0 * alpha, res[5], res[2]));
+            const double sd = __fma_rn(-alpha, res[7], res[3]);
+            const double dd = __fma_rn(alpha * alpha, res[9], __fma_rn(-2.0 * alpha, res[8], res[4]));
+            beta = rho_next / rho;
+            rho = rho_next;
+            eta = 0.0;
+            if (dd > 0.0) {
+                eta = -sd / dd;
+                eta = eta < 0.0 ? 0.0 : (1.0 < eta ? 1.0 : eta);
             }
-            STAMP(5)
-            double res[1];
-            barrier_reduce<1>(v, bar, a.part, gen, sm, &sm_flag, res);  // also publishes p (halo)
-            snorm = sqrt(res[0]);
-            STAMP(6)
+            ++iter;
         }
-        ++iter;
-        if (blockIdx.x == 0 && t == 0 && iter < a.hist_cap) a.hist[iter] = snorm;
     }
 #undef STAMP
 #undef DCO_OK
 #undef KO
     // publish xs for the final objective's stencil, dense map
     for (int i = base + t; i < base + size; i += THREADS) {
-        double xsi = sx[chunk + (i - base)];  // s_xs
+        double xsi = sx[2 * w + chunk + (i - base)];  // s_xs
         a.xs[i] = xsi;
         a.dense[i] = static_cast<float>(dmax0(xsi));
     }
     {
         double z[1] = {0.0}, dummy[1];
-        barrier_reduce<1>(z, bar, a.part, gen, sm, &sm_flag, dummy);  // xs visible grid-wide
+        barrier_reduce<1>(z, bar, a.part, gen, sm, dummy);  // xs visible grid-wide
     }
     double o[2] = {0.0, 0.0};
     for (int i = base + t; i < base + size; i += THREADS) {
@@ -902,7 +865,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
         o[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
         o[1] += a.rhs[i] * xsi;
     }
-    barrier_reduce<2>(o, bar, a.part, gen, sm, &sm_flag, o);
+    barrier_reduce<2>(o, bar, a.part, gen, sm, o);
     if (blockIdx.x == 0 && t == 0) {
         a.out->objective_final = o[0] - 2.0 * o[1] + cterm;
         a.out->status = 0;
@@ -915,21 +878,23 @@ inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + 
 
 int g_pcg_blocks = 0;
 long long* g_pcg_dbg = nullptr;
+constexpr int kDbgLen = 1280 + 64 * 1024 * 3;  // + per-block globaltimer stamps
 int g_sms = 0;
 
 typedef void (*OnchipKernel)(CGArgs, int, GridBar*);
 constexpr int kOnchipThreadsUsed = 1024;
-OnchipKernel onchip_for(int ept, int* ept_used) {
-    *ept_used = ept;
+constexpr int kOnchipSmemMax = 222 * 1024;  // + 2.6 KB static reduction scratch <= 227 KB
+OnchipKernel onchip_for(int threads, int ept) {
+    if (threads != 1024) return nullptr;
     switch (ept) {
-        case 1: return k_pcg_onchip<1, kOnchipThreadsUsed>;
-        case 2: return k_pcg_onchip<2, kOnchipThreadsUsed>;
-        case 3: return k_pcg_onchip<3, kOnchipThreadsUsed>;
-        case 4: return k_pcg_onchip<4, kOnchipThreadsUsed>;
-        case 5: return k_pcg_onchip<5, kOnchipThreadsUsed>;
-        case 6: return k_pcg_onchip<6, kOnchipThreadsUsed>;
-        case 7: return k_pcg_onchip<7, kOnchipThreadsUsed>;
-        case 8: return k_pcg_onchip<8, kOnchipThreadsUsed>;
+        case 1: return k_pcg_onchip<1, 1024>;
+        case 2: return k_pcg_onchip<2, 1024>;
+        case 3: return k_pcg_onchip<3, 1024>;
+        case 4: return k_pcg_onchip<4, 1024>;
+        case 5: return k_pcg_onchip<5, 1024>;
+        case 6: return k_pcg_onchip<6, 1024>;
+        case 7: return k_pcg_onchip<7, 1024>;
+        case 8: return k_pcg_onchip<8, 1024>;
         default: return nullptr;
     }
 }
@@ -1058,7 +1023,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     a.dbg = nullptr;
     if (getenv("DCO_PCG_DEBUG")) {
         static long long* dbg = nullptr;
-        if (!dbg) cuda_check(cudaMalloc(&dbg, 1280 * sizeof(long long)), "dbg");
+        if (!dbg) cuda_check(cudaMalloc(&dbg, kDbgLen * sizeof(long long)), "dbg");
         a.dbg = dbg;
         g_pcg_dbg = dbg;
     }
@@ -1066,14 +1031,15 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     // per block with 4 doubles each in shared memory, <= 8 per thread
     const int sms = g_sms ? g_sms : (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, ctx->device), g_sms);
     const int chunk = static_cast<int>((n + sms - 1) / sms);
-    int ept = (chunk + kOnchipThreadsUsed - 1) / kOnchipThreadsUsed;
-    const size_t smem = static_cast<size_t>(chunk) * 4 * sizeof(double);
-    OnchipKernel kern = onchip_for(ept, &ept);
-    if (kern && smem <= 200 * 1024 && sms <= 1024) {
+    const int threads = kOnchipThreadsUsed;
+    const int ept = (chunk + threads - 1) / threads;
+    const size_t smem = (static_cast<size_t>(chunk) * 4 + 2 * static_cast<size_t>(w)) * sizeof(double);
+    OnchipKernel kern = onchip_for(threads, ept);
+    if (kern && smem <= kOnchipSmemMax && sms <= 1024) {
         static bool attr[17] = {};
         if (!attr[ept]) {
             cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kOnchipSmemMax),
                        "smem attr");
             attr[ept] = true;
         }
@@ -1081,7 +1047,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
         cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
         void* params[] = {&a, &chunk_arg, &bar};
-        launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(kOnchipThreadsUsed),
+        launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(threads),
                                       params, smem);
         launched(ctx, "k_pcg_onchip");
         return;

@@ -21,17 +21,32 @@ for i in range(4):
     s.push_gray8(torch.from_numpy(l8).cuda(), torch.from_numpy(r8).cuda(), want_result=False)
 torch.cuda.synchronize()
 lib = native.load()
-buf = (ctypes.c_longlong * 1280)()
-lib.dco_debug_pcg_stamps(buf, 1280)
+NB = torch.cuda.get_device_properties(0).multi_processor_count
+LEN = 1280 + 64 * 1024 * 3
+buf = (ctypes.c_longlong * LEN)()
+lib.dco_debug_pcg_stamps(buf, LEN)
+g = np.array(buf[1280:]).reshape(64, 1024, 3)[:, :NB, :].astype(np.float64)
 a = np.array(buf[:640]).reshape(64, 10)
-b = np.array(buf[640:]).reshape(64, 10)
-names = ["A work", "A barrier-reduce", "B work", "B barrier-reduce", "C work", "C barrier-reduce"]
+b = np.array(buf[640:1280]).reshape(64, 10)
+names = ["A (MR tail + SpMV) work", "A barrier-reduce", "B work", "B barrier-reduce"]
 for tag, m in (("block0", a), ("last", b)):
-    d = np.diff(m[5:40, :7], axis=1).mean(axis=0)
+    d = np.diff(m[5:40, :5], axis=1).mean(axis=0)
     tot = (m[6:40, 0] - m[5:39, 0]).mean()
     print(tag, "cycles/iter %.0f" % tot)
     for n, v in zip(names, d):
-        print("   %-16s %8.0f" % (n, v))
-    e = m[5:40]
-    print("   B: work-end->arrive %.0f  atomic %.0f  arrive->released %.0f  released->B-end %.0f" % (
-        (e[:, 7] - e[:, 3]).mean(), (e[:, 8] - e[:, 7]).mean(), (e[:, 9] - e[:, 8]).mean(), (e[:, 4] - e[:, 9]).mean()))
+        print("   %-24s %8.0f" % (n, v))
+
+# per-block globaltimer (ns): work duration, arrival skew, release latency
+it = slice(5, 40)
+work = (g[it, :, 1] - g[it, :, 0])
+arr = g[it, :, 1] - g[it, :, 1].min(axis=1, keepdims=True)
+rel = g[it, :, 2] - g[it, :, 1].max(axis=1, keepdims=True)
+per_iter = np.diff(g[4:40, :, 0].min(axis=1))
+print("ns/iter %.0f" % per_iter.mean())
+print("work ns: mean %.0f min %.0f max %.0f" % (work.mean(), work.mean(0).min(), work.mean(0).max()))
+print("arrival skew ns (last - first): %.0f" % (arr.max(axis=1).mean()))
+print("release after last arrival ns: mean %.0f max %.0f" % (rel.mean(), rel.max(axis=1).mean()))
+wm = work.mean(0)
+order = np.argsort(-wm)
+print("slowest blocks:", [(int(b), int(wm[b])) for b in order[:8]])
+print("fastest blocks:", [(int(b), int(wm[b])) for b in order[-4:]])
