@@ -371,6 +371,258 @@ __global__ void k_agg_vpass(const double* __restrict__ hsum, int w, int h, int n
     }
 }
 
+// Packed per-pixel arm words for the pipelined passes below:
+// hinfo = left | right << 8; vinfo = up | down << 8 | region << 16 (region
+// < 65536 whenever every arm <= 127, which the host checks).
+__global__ void k_region_pack(const uint8_t* __restrict__ L, const uint8_t* __restrict__ R,
+                              const uint8_t* __restrict__ U, const uint8_t* __restrict__ D, int w, int h,
+                              uint32_t* __restrict__ hinfo, uint32_t* __restrict__ vinfo) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    size_t i = static_cast<size_t>(y) * w + x;
+    int s = 0;
+    for (int yy = y - U[i]; yy <= y + D[i]; ++yy) {
+        size_t j = static_cast<size_t>(yy) * w + x;
+        s += L[j] + R[j] + 1;
+    }
+    hinfo[i] = L[i] | (static_cast<uint32_t>(R[i]) << 8);
+    vinfo[i] = U[i] | (static_cast<uint32_t>(D[i]) << 8) | (static_cast<uint32_t>(s) << 16);
+}
+
+// Pipelined horizontal pass: same chain and rounding as k_agg_hpass. Block
+// = 32 slices x 4 rows (kAggThreads). The per-thread prefix ring holds
+// exactly 2*l1+2 entries (modular slots, so more blocks fit per SM); the
+// costs and the arm words of the next kPF steps are in flight while the
+// current kPF steps execute; chunks away from the borders run without
+// per-step bounds checks.
+constexpr int kAggThreads = 128;
+
+template <int kPF>
+__global__ void __launch_bounds__(kAggThreads) k_agg_h2(const float* __restrict__ cost, int w, int h, int nd,
+                                                        const uint32_t* __restrict__ hinfo, int lag, int ring_n,
+                                                        double* __restrict__ hsum) {
+    extern __shared__ double ring[];
+    const int lane = threadIdx.x, tid = threadIdx.y * 32 + threadIdx.x;
+    const int k = blockIdx.x * 32 + lane;
+    const int y = blockIdx.y * 4 + threadIdx.y;
+    if (y >= h || k >= nd) return;
+    const float* lp = cost + static_cast<size_t>(y) * w * nd + k;  // next cost to load
+    double* dst = hsum + static_cast<size_t>(y) * w * nd + k;
+    const uint32_t* info = hinfo + static_cast<size_t>(y) * w;
+    double* rg = ring + tid;
+    double P = 0.0;
+    rg[0] = 0.0;
+    int s1 = 0;  // slot of P[x + 1] after step x
+    float cur[kPF], nxt[kPF];
+    uint32_t ci[kPF], ni[kPF];
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) {
+        cur[j] = j < w ? __ldg(lp) : 0.0f;
+        lp += nd;
+        const int px = j + 1 - lag;
+        ci[j] = (px >= 0 && px < w) ? __ldg(info + px) : 0u;
+    }
+    auto step = [&](int x, float c, uint32_t v) {
+        P += static_cast<double>(c);
+        s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
+        rg[s1 * kAggThreads] = P;
+        const int l = v & 255u, r = (v >> 8) & 255u;
+        int ib = s1 + r + 1 - lag;  // P[px + r + 1]
+        ib += ib < 0 ? ring_n : 0;
+        int ia = s1 - lag - l;  // P[px - l]
+        ia += ia < 0 ? ring_n : 0;
+        return rg[ib * kAggThreads] - rg[ia * kAggThreads];
+    };
+    for (int x0 = 0; x0 < w; x0 += kPF) {
+        const bool fast = x0 + 2 * kPF <= w && x0 + 1 - lag >= 0;
+        if (fast) {
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                nxt[j] = __ldg(lp);
+                lp += nd;
+                ni[j] = __ldg(info + x0 + kPF + j + 1 - lag);
+            }
+            const int sb = s1;
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                P += static_cast<double>(cur[j]);
+                s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
+                rg[s1 * kAggThreads] = P;
+            }
+            double* dp = dst + static_cast<size_t>(x0 + 1 - lag) * nd;
+            int sj = sb;
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                sj = (sj + 1 == ring_n) ? 0 : sj + 1;  // slot of P[x0 + j + 1]
+                const uint32_t v = ci[j];
+                const int l = v & 255u, r = (v >> 8) & 255u;
+                int ib = sj + r + 1 - lag;
+                ib += ib < 0 ? ring_n : 0;
+                int ia = sj - lag - l;
+                ia += ia < 0 ? ring_n : 0;
+                *dp = rg[ib * kAggThreads] - rg[ia * kAggThreads];
+                dp += nd;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                const int x = x0 + kPF + j;
+                nxt[j] = x < w ? __ldg(lp) : 0.0f;
+                lp += nd;
+                const int px = x + 1 - lag;
+                ni[j] = (px >= 0 && px < w) ? __ldg(info + px) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                const int x = x0 + j;
+                if (x < w) {
+                    const int px = x + 1 - lag;
+                    if (px >= 0) {
+                        dst[static_cast<size_t>(px) * nd] = step(x, cur[j], ci[j]);
+                    } else {
+                        P += static_cast<double>(cur[j]);
+                        s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
+                        rg[s1 * kAggThreads] = P;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            cur[j] = nxt[j];
+            ci[j] = ni[j];
+        }
+    }
+    // s1 = slot of P[w]
+    for (int px = max(w + 1 - lag, 0); px < w; ++px) {
+        const uint32_t v = info[px];
+        const int l = v & 255u, r = (v >> 8) & 255u;
+        int ib = s1 + (px + r + 1 - w);
+        ib += ib < 0 ? ring_n : 0;
+        int ia = s1 + (px - l - w);
+        ia += ia < 0 ? ring_n : 0;
+        dst[static_cast<size_t>(px) * nd] = rg[ib * kAggThreads] - rg[ia * kAggThreads];
+    }
+}
+
+// Pipelined vertical pass: same chain, rounding and division as k_agg_vpass.
+// Block = 32 slices x 4 columns.
+template <int kPF>
+__global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict__ hsum, int w, int h, int nd,
+                                                        const uint32_t* __restrict__ vinfo, int lag, int ring_n,
+                                                        float* __restrict__ out) {
+    extern __shared__ double ring[];
+    const int lane = threadIdx.x, tid = threadIdx.y * 32 + threadIdx.x;
+    const int k = blockIdx.x * 32 + lane;
+    const int x = blockIdx.y * 4 + threadIdx.y;
+    if (x >= w || k >= nd) return;
+    const size_t row = static_cast<size_t>(w) * nd;
+    const double* lp = hsum + static_cast<size_t>(x) * nd + k;
+    float* dst = out + static_cast<size_t>(x) * nd + k;
+    const uint32_t* info = vinfo + x;
+    double* rg = ring + tid;
+    double C = 0.0;
+    rg[0] = 0.0;
+    int s1 = 0;
+    double cur[kPF], nxt[kPF];
+    uint32_t ci[kPF], ni[kPF];
+#pragma unroll
+    for (int j = 0; j < kPF; ++j) {
+        cur[j] = j < h ? __ldg(lp) : 0.0;
+        lp += row;
+        const int py = j + 1 - lag;
+        ci[j] = (py >= 0 && py < h) ? __ldg(info + static_cast<size_t>(py) * w) : 0u;
+    }
+    auto step = [&](double c, uint32_t v) {
+        C += c;
+        s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
+        rg[s1 * kAggThreads] = C;
+        const int u = v & 255u, d = (v >> 8) & 255u;
+        int ib = s1 + d + 1 - lag;
+        ib += ib < 0 ? ring_n : 0;
+        int ia = s1 - lag - u;
+        ia += ia < 0 ? ring_n : 0;
+        const double total = rg[ib * kAggThreads] - rg[ia * kAggThreads];
+        return static_cast<float>(total / static_cast<int>(v >> 16));
+    };
+    for (int y0 = 0; y0 < h; y0 += kPF) {
+        const bool fast = y0 + 2 * kPF <= h && y0 + 1 - lag >= 0;
+        if (fast) {
+            const uint32_t* ip = info + static_cast<size_t>(y0 + kPF + 1 - lag) * w;
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                nxt[j] = __ldg(lp);
+                lp += row;
+                ni[j] = __ldg(ip);
+                ip += w;
+            }
+            // prefixes of the whole chunk first, then its kPF outputs: no
+            // shared-memory store sits between two outputs' loads
+            const int sb = s1;
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                C += cur[j];
+                s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
+                rg[s1 * kAggThreads] = C;
+            }
+            float* dp = dst + static_cast<size_t>(y0 + 1 - lag) * row;
+            int sj = sb;
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                sj = (sj + 1 == ring_n) ? 0 : sj + 1;  // slot of C[y0 + j + 1]
+                const uint32_t v = ci[j];
+                const int u = v & 255u, d = (v >> 8) & 255u;
+                int ib = sj + d + 1 - lag;
+                ib += ib < 0 ? ring_n : 0;
+                int ia = sj - lag - u;
+                ia += ia < 0 ? ring_n : 0;
+                const double total = rg[ib * kAggThreads] - rg[ia * kAggThreads];
+                *dp = static_cast<float>(total / static_cast<int>(v >> 16));
+                dp += row;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                const int y = y0 + kPF + j;
+                nxt[j] = y < h ? __ldg(lp) : 0.0;
+                lp += row;
+                const int py = y + 1 - lag;
+                ni[j] = (py >= 0 && py < h) ? __ldg(info + static_cast<size_t>(py) * w) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < kPF; ++j) {
+                const int y = y0 + j;
+                if (y < h) {
+                    const int py = y + 1 - lag;
+                    if (py >= 0) {
+                        dst[py * row] = step(cur[j], ci[j]);
+                    } else {
+                        C += cur[j];
+                        s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
+                        rg[s1 * kAggThreads] = C;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+            cur[j] = nxt[j];
+            ci[j] = ni[j];
+        }
+    }
+    for (int py = max(h + 1 - lag, 0); py < h; ++py) {
+        const uint32_t v = info[static_cast<size_t>(py) * w];
+        const int u = v & 255u, d = (v >> 8) & 255u;
+        int ib = s1 + (py + d + 1 - h);
+        ib += ib < 0 ? ring_n : 0;
+        int ia = s1 + (py - u - h);
+        ia += ia < 0 ? ring_n : 0;
+        const double total = rg[ib * kAggThreads] - rg[ia * kAggThreads];
+        dst[py * row] = static_cast<float>(total / static_cast<int>(v >> 16));
+    }
+}
+
 // ------------------------------------------------------------------- WTA ---
 // select_disparity_wta, stereo.cpp:220-238: first strict minimum. One warp
 // per pixel; lanes stride over d and the warp reduces (cost, d) with ties to
@@ -1039,14 +1291,43 @@ void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, cons
                      const uint8_t* r, const uint8_t* u, const uint8_t* d, int max_arm,
                      float* out) {
     require(nd >= 1, "aggregate_costs: empty disparity range");
+    require(max_arm >= 0 && max_arm <= 255, "aggregate_costs: arm length out of range");
     const size_t n = static_cast<size_t>(w) * h;
-    int* region = static_cast<int*>(scratch(ctx, S_REGION, n * sizeof(int)));
     double* hsum = static_cast<double*>(scratch(ctx, S_HSUM, n * nd * sizeof(double)));
+    const int lag = max_arm + 1;
     dim3 b(32, 8);
+    if (max_arm <= 127) {
+        // packed arm words (region < 65536), exact-size modular rings
+        uint32_t* hinfo = static_cast<uint32_t*>(scratch(ctx, S_REGION, 2 * n * sizeof(uint32_t)));
+        uint32_t* vinfo = hinfo + n;
+        k_region_pack<<<grid2(w, h, b), b, 0, ctx->stream>>>(l, r, u, d, w, h, hinfo, vinfo);
+        launched(ctx, "k_region_pack");
+        constexpr int kVPF = 8, kHPF = 16;
+        // a chunk's prefixes are all written before its outputs read the ring
+        const int ring_h = 2 * max_arm + 2 + kHPF - 1, ring_v = 2 * max_arm + 2 + kVPF - 1;
+        dim3 tb(32, 4);
+        const size_t smem_h = static_cast<size_t>(ring_h) * kAggThreads * sizeof(double);
+        const size_t smem_v = static_cast<size_t>(ring_v) * kAggThreads * sizeof(double);
+        static bool attr2 = false;
+        if (!attr2) {
+            cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cudaFuncSetAttribute(k_agg_v2<kVPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            cudaFuncSetAttribute(k_agg_v2<kVPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            attr2 = true;
+        }
+        k_agg_h2<kHPF><<<dim3((nd + 31) / 32, (h + 3) / 4), tb, smem_h, ctx->stream>>>(cost, w, h, nd, hinfo, lag,
+                                                                                      ring_h, hsum);
+        launched(ctx, "k_agg_h2");
+        k_agg_v2<kVPF><<<dim3((nd + 31) / 32, (w + 3) / 4), tb, smem_v, ctx->stream>>>(hsum, w, h, nd, vinfo, lag,
+                                                                                      ring_v, out);
+        launched(ctx, "k_agg_v2");
+        return;
+    }
+    int* region = static_cast<int*>(scratch(ctx, S_REGION, n * sizeof(int)));
     k_region_size<<<grid2(w, h, b), b, 0, ctx->stream>>>(l, r, u, d, w, h, region);
     launched(ctx, "k_region_size");
-    require(max_arm >= 0 && max_arm <= 255, "aggregate_costs: arm length out of range");
-    const int lag = max_arm + 1, ring = ring_size(max_arm);
+    const int ring = ring_size(max_arm);
     int rows = 4;
     while (rows > 1 && static_cast<size_t>(ring) * 32 * rows * sizeof(double) > 200 * 1024) rows >>= 1;
     dim3 tb(32, rows);

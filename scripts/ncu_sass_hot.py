@@ -11,7 +11,8 @@ def main(path, kernel, top=30):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[1]
     si, wi = hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
-    data = [r for r in rows[2:] if len(r) == len(hdr)]
+    data = [r for r in rows[2:] if len(r) == len(hdr) and r[wi] != hdr[wi]]
+    data = [r for r in data if r[wi].replace(".", "", 1).isdigit() or r[wi] == ""]
     tot = sum(float(r[wi] or 0) for r in data)
     print("total samples", tot)
     for idx, r in sorted(enumerate(data), key=lambda x: -float(x[1][wi] or 0))[:top]:
