@@ -4,7 +4,7 @@
 // Per pyramid level three kernels run, for BOTH directions of the pipeline's
 // bidirectional flow at once (blockIdx.z = direction; the `from` pyramid is
 // shared): the flow upsample from the coarser level (flow.cpp:39-62), one
-// thread per 8x8 patch for the 12-step inverse-compositional Gauss-Newton
+// warp per 8x8 patch for the 12-step inverse-compositional Gauss-Newton
 // search (flow.cpp:72-121, double sums in the reference's (dy,dx) order), and
 // one thread per pixel gathering the weighted patch mean in the reference's
 // (py,px) patch order (flow.cpp:123-160). Arithmetic order matches the
@@ -88,52 +88,73 @@ __global__ void k_flow_upsample(const float* __restrict__ cu, const float* __res
     fv[o] = 2.0f * (tv * (1 - fy) + bv * fy);
 }
 
-// search_patch, flow.cpp:72-121. One thread per patch; z = direction. The
-// template t and its gradients gx, gy (fixed for the 12 iterations) are kept
-// in shared memory ([n][thread], conflict-free) instead of 192 registers.
-constexpr int kPatchThreads = 64;
+// search_patch, flow.cpp:72-121, one WARP per patch; z = direction. Lanes
+// own samples n = lane and lane + 32 (the 64 bilinear samples of an
+// iteration run in parallel); every product gx*r, gy*r, r*r of two floats is
+// exact in double, so the reference's sequential sums are reproduced by
+// lanes 0, 1, 2 adding the exact terms in (dy, dx) order -- the same three
+// rounding chains, run side by side.
+constexpr int kPatchWarps = 4;
 
-__global__ void __launch_bounds__(kPatchThreads) k_flow_patch(const float* __restrict__ from,
-                                                              const float* __restrict__ to0,
-                                                              const float* __restrict__ to1, int w, int h, int nx,
-                                                              int ny, const float* __restrict__ init_u_base,
-                                                              const float* __restrict__ init_v_base,
-                                                              size_t field_stride, float* __restrict__ res_base,
-                                                              size_t res_stride) {
-    __shared__ float s_t[kPatch * kPatch * kPatchThreads];
-    __shared__ float s_gx[kPatch * kPatch * kPatchThreads];
-    __shared__ float s_gy[kPatch * kPatch * kPatchThreads];
-    const int tid = threadIdx.x;
-    int j = blockIdx.x * blockDim.x + tid;
-    if (j >= nx * ny) return;
+__global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* __restrict__ from,
+                                                                  const float* __restrict__ to0,
+                                                                  const float* __restrict__ to1, int w, int h,
+                                                                  int nx, int ny,
+                                                                  const float* __restrict__ init_u_base,
+                                                                  const float* __restrict__ init_v_base,
+                                                                  size_t field_stride, float* __restrict__ res_base,
+                                                                  size_t res_stride) {
+    constexpr int N = kPatch * kPatch;
+    __shared__ float s_t[kPatchWarps][N];
+    __shared__ float s_gx[kPatchWarps][N];
+    __shared__ float s_gy[kPatchWarps][N];
+    __shared__ double s_term[kPatchWarps][3][N];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int j = blockIdx.x * kPatchWarps + wp;
+    if (j >= nx * ny) return;  // warp-uniform
     const float* to = blockIdx.z ? to1 : to0;
     const float* iu = init_u_base + blockIdx.z * field_stride;
     const float* iv = init_v_base + blockIdx.z * field_stride;
     float* res = res_base + blockIdx.z * res_stride;
-    int jy = j / nx, jx = j - jy * nx;
-    int px = patch_pos(jx, nx, w), py = patch_pos(jy, ny, h);
-    int cx = min(px + kPatch / 2, w - 1), cy = min(py + kPatch / 2, h - 1);
+    const int jy = j / nx, jx = j - jy * nx;
+    const int px = patch_pos(jx, nx, w), py = patch_pos(jy, ny, h);
+    const int cx = min(px + kPatch / 2, w - 1), cy = min(py + kPatch / 2, h - 1);
     const float seed_u = iu[static_cast<size_t>(cy) * w + cx];
     const float seed_v = iv[static_cast<size_t>(cy) * w + cx];
+    float* t = s_t[wp];
+    float* gxs = s_gx[wp];
+    float* gys = s_gy[wp];
+    double* term = &s_term[wp][0][0];
 
-    double h00 = 1e-6, h01 = 0.0, h11 = 1e-6;
-#pragma unroll 8
-    for (int n = 0; n < kPatch * kPatch; ++n) {
-        int dy = n >> 3, dx = n & 7;
-        int y = py + dy, x = px + dx;
-        int ym = max(y - 1, 0), yp = min(y + 1, h - 1);
-        int xm = max(x - 1, 0), xp = min(x + 1, w - 1);
+    // template, gradients and the Hessian terms (flow.cpp:78-89)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        const int n = lane + 32 * half;
+        const int y = py + (n >> 3), x = px + (n & 7);
+        const int ym = max(y - 1, 0), yp = min(y + 1, h - 1);
+        const int xm = max(x - 1, 0), xp = min(x + 1, w - 1);
         const float* row = from + static_cast<size_t>(y) * w;
-        float t = __ldg(row + x);
-        float gx = 0.5f * (__ldg(row + xp) - __ldg(row + xm));
-        float gy = 0.5f * (__ldg(from + static_cast<size_t>(yp) * w + x) - __ldg(from + static_cast<size_t>(ym) * w + x));
-        s_t[n * kPatchThreads + tid] = t;
-        s_gx[n * kPatchThreads + tid] = gx;
-        s_gy[n * kPatchThreads + tid] = gy;
-        h00 += static_cast<double>(gx) * gx;
-        h01 += static_cast<double>(gx) * gy;
-        h11 += static_cast<double>(gy) * gy;
+        const float tv = __ldg(row + x);
+        const float gx = 0.5f * (__ldg(row + xp) - __ldg(row + xm));
+        const float gy =
+            0.5f * (__ldg(from + static_cast<size_t>(yp) * w + x) - __ldg(from + static_cast<size_t>(ym) * w + x));
+        t[n] = tv;
+        gxs[n] = gx;
+        gys[n] = gy;
+        term[0 * N + n] = static_cast<double>(gx) * gx;
+        term[1 * N + n] = static_cast<double>(gx) * gy;
+        term[2 * N + n] = static_cast<double>(gy) * gy;
     }
+    __syncwarp();
+    double acc = (lane == 1) ? 0.0 : 1e-6;  // h00, h01, h11 on lanes 0, 1, 2
+    if (lane < 3) {
+        const double* tl = term + lane * N;
+#pragma unroll 16
+        for (int n = 0; n < N; ++n) acc += tl[n];
+    }
+    const double h00 = __shfl_sync(0xffffffffu, acc, 0);
+    const double h01 = __shfl_sync(0xffffffffu, acc, 1);
+    const double h11 = __shfl_sync(0xffffffffu, acc, 2);
     const double det = h00 * h11 - h01 * h01;
     const double inv00 = h11 / det, inv01 = -h01 / det, inv11 = h00 / det;
 
@@ -141,26 +162,30 @@ __global__ void __launch_bounds__(kPatchThreads) k_flow_patch(const float* __res
     double mse = 0.0;
     const float fw = static_cast<float>(w), fh = static_cast<float>(h);
     for (int iter = 0; iter < kIters; ++iter) {
-        // all 64 residuals first (independent samples: full ILP), then the
-        // three sums in the reference's sequential (dy, dx) order
-        float rr[kPatch * kPatch];
+        __syncwarp();  // previous iteration's term reads are done
 #pragma unroll
-        for (int n = 0; n < kPatch * kPatch; ++n) {
-            float sx = static_cast<float>(px + (n & 7)) + u;
-            float sy = static_cast<float>(py + (n >> 3)) + v;
-            rr[n] = sample_bilinear(to, w, h, sx, sy) - s_t[n * kPatchThreads + tid];
+        for (int half = 0; half < 2; ++half) {
+            const int n = lane + 32 * half;
+            const float sx = static_cast<float>(px + (n & 7)) + u;
+            const float sy = static_cast<float>(py + (n >> 3)) + v;
+            const float r = sample_bilinear(to, w, h, sx, sy) - t[n];
+            term[0 * N + n] = static_cast<double>(gxs[n]) * r;
+            term[1 * N + n] = static_cast<double>(gys[n]) * r;
+            term[2 * N + n] = static_cast<double>(r) * r;
         }
-        double bu = 0.0, bv = 0.0, sse = 0.0;
-#pragma unroll
-        for (int n = 0; n < kPatch * kPatch; ++n) {
-            float r = rr[n];
-            bu += static_cast<double>(s_gx[n * kPatchThreads + tid]) * r;
-            bv += static_cast<double>(s_gy[n * kPatchThreads + tid]) * r;
-            sse += static_cast<double>(r) * r;
+        __syncwarp();
+        double sum = 0.0;  // bu, bv, sse on lanes 0, 1, 2
+        if (lane < 3) {
+            const double* tl = term + lane * N;
+#pragma unroll 16
+            for (int n = 0; n < N; ++n) sum += tl[n];
         }
+        const double bu = __shfl_sync(0xffffffffu, sum, 0);
+        const double bv = __shfl_sync(0xffffffffu, sum, 1);
+        const double sse = __shfl_sync(0xffffffffu, sum, 2);
         mse = sse / (kPatch * kPatch);
-        double step_u = inv00 * bu + inv01 * bv;
-        double step_v = inv01 * bu + inv11 * bv;
+        const double step_u = inv00 * bu + inv01 * bv;
+        const double step_v = inv01 * bu + inv11 * bv;
         u -= static_cast<float>(step_u);
         v -= static_cast<float>(step_v);
         if (!isfinite(u) || !isfinite(v)) {
@@ -172,9 +197,11 @@ __global__ void __launch_bounds__(kPatchThreads) k_flow_patch(const float* __res
         v = clampf(v, -fh, fh);
         if (step_u * step_u + step_v * step_v < 1e-6) break;
     }
-    res[3 * j + 0] = u;
-    res[3 * j + 1] = v;
-    res[3 * j + 2] = static_cast<float>(1.0 / (mse + 1e-2));
+    if (lane == 0) {
+        res[3 * j + 0] = u;
+        res[3 * j + 1] = v;
+        res[3 * j + 2] = static_cast<float>(1.0 / (mse + 1e-2));
+    }
 }
 
 // estimate_level gather, flow.cpp:137-160: per pixel, the double-weighted mean
@@ -326,10 +353,10 @@ void compute_flow_multi(dco_ctx* ctx, const float* from, const float* const* to,
             cur ^= 1;
         }
         int np = L.nx * L.ny;
-        k_flow_patch<<<dim3(blocks_for(np, kPatchThreads), 1, dirs), kPatchThreads, 0, ctx->stream>>>(
+        k_flow_patch_w<<<dim3((np + kPatchWarps - 1) / kPatchWarps, 1, dirs), kPatchWarps * 32, 0, ctx->stream>>>(
             p_from[l], p_to[0][l], dirs > 1 ? p_to[1][l] : p_to[0][l], L.w, L.h, L.nx, L.ny, U(cur, 0), V(cur, 0), fs, res,
             max_patches * 3);
-        launched(ctx, "k_flow_patch");
+        launched(ctx, "k_flow_patch_w");
         cuda_check(cudaMemsetAsync(uncovered, 0, sizeof(int), ctx->stream), "memset");
         k_flow_gather<<<grid2(L.w, L.h, b, dirs), b, 0, ctx->stream>>>(
             res, max_patches * 3, L.w, L.h, L.nx, L.ny, U(cur ^ 1, 0), V(cur ^ 1, 0), fs, uncovered);
