@@ -843,141 +843,11 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_refine_thread(
 // histogram of stereo.cpp:252-297 is the cross-region sum of one-hot bins):
 //   H(x, y', v) = #{c in the horizontal span of (x, y') : bin(c, y') == v}
 //   count(x, y, v) = sum over y' on the vertical arm of (x, y) of H(x, y', v)
-// Counts are integers, so any summation order is exact. Pass 1 builds per-row
-// bitmasks (one per bin) and popcounts each span; pass 2 walks each column
-// with a prefix ring and takes the mode (max count, smallest bin on ties)
-// with warp shuffles. Cost O(N * bins) instead of O(N * region) — regions
-// reach 35x35 on smooth texture.
-__global__ void k_refine_hcount(const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ L,
-                                const uint8_t* __restrict__ R, int nbp /* padded bins */,
-                                uint8_t* __restrict__ hcnt /* [y][x][nbp] */) {
-    extern __shared__ unsigned masks[];  // [nbp][words]
-    const int y = blockIdx.x;
-    const int words = (w + 31) >> 5;
-    for (int i = threadIdx.x; i < nbp * words; i += blockDim.x) masks[i] = 0u;
-    __syncthreads();
-    const float* row = cur + static_cast<size_t>(y) * w;
-    for (int x = threadIdx.x; x < w; x += blockDim.x) {
-        float v = row[x];
-        if (isfinite(v)) {
-            int b = min(max(static_cast<int>(lroundf(v)), 0), nbp - 1);
-            atomicOr(&masks[b * words + (x >> 5)], 1u << (x & 31));
-        }
-    }
-    __syncthreads();
-    const uint8_t* Lr = L + static_cast<size_t>(y) * w;
-    const uint8_t* Rr = R + static_cast<size_t>(y) * w;
-    uint8_t* out = hcnt + static_cast<size_t>(y) * w * nbp;
-    for (int e = threadIdx.x; e < w * nbp; e += blockDim.x) {
-        const int x = e / nbp, b = e - x * nbp;
-        const int a = x - Lr[x], z = x + Rr[x];  // inclusive span [a, z]
-        const unsigned* m = masks + b * words;
-        int cnt = 0;
-        for (int wd = a >> 5; wd <= (z >> 5); ++wd) {
-            unsigned bits = m[wd];
-            int lo = max(a - (wd << 5), 0), hi = min(z - (wd << 5), 31);
-            unsigned sel = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
-            cnt += __popc(bits & sel);
-        }
-        out[e] = static_cast<uint8_t>(cnt);
-    }
-}
-
-template <int VPL>  // bins per lane (nbp = 32 * VPL)
-__global__ void k_refine_vmode(const float* __restrict__ cur, const uint8_t* __restrict__ hcnt, int w, int h,
-                               const uint8_t* __restrict__ U, const uint8_t* __restrict__ D, int lag, int ring_mask,
-                               float* __restrict__ next) {
-    extern __shared__ unsigned short rings[];  // per warp: [ring][32 lanes][VPL]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int x = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (x >= w) return;
-    const int nbp = 32 * VPL;
-    const int ring = ring_mask + 1;
-    unsigned short* rg = rings + static_cast<size_t>(warp) * ring * 32 * VPL;
-    auto R_at = [&](int slot, int j) -> unsigned short& { return rg[(slot * 32 + lane) * VPL + j]; };
-    unsigned short C[VPL];
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-        C[j] = 0;
-        R_at(0, j) = 0;
-    }
-    auto finalize = [&](int py) {
-        const size_t i = static_cast<size_t>(py) * w + x;
-        const float center = cur[i];
-        const int a = py - U[i], b = py + D[i] + 1;
-        int best_c = 0, best_b = 0x7fffffff, total = 0;
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-            int cnt = static_cast<int>(R_at(b & ring_mask, j)) - static_cast<int>(R_at(a & ring_mask, j));
-            int bin = lane * VPL + j;
-            total += cnt;
-            if (cnt > best_c) {  // ascending bins within the lane: first max kept
-                best_c = cnt;
-                best_b = bin;
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            total += __shfl_xor_sync(0xffffffffu, total, off);
-            int oc = __shfl_xor_sync(0xffffffffu, best_c, off);
-            int ob = __shfl_xor_sync(0xffffffffu, best_b, off);
-            if (oc > best_c || (oc == best_c && ob < best_b)) {
-                best_c = oc;
-                best_b = ob;
-            }
-        }
-        if (lane == 0) {
-            float o = center;  // removed outliers stay removed
-            if (isfinite(center))
-                o = (best_c == 1 && total >= 4) ? __int_as_float(0x7fc00000) : static_cast<float>(best_b);
-            next[i] = o;
-        }
-    };
-    const size_t rowstride = static_cast<size_t>(w) * nbp;
-    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
-    for (int y = 0; y < h; ++y) {
-        const uint8_t* hp = src + y * rowstride;
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-            C[j] = static_cast<unsigned short>(C[j] + hp[j]);
-            R_at((y + 1) & ring_mask, j) = C[j];
-        }
-        __syncwarp();
-        const int py = y + 1 - lag;
-        if (py >= 0) finalize(py);
-        __syncwarp();
-    }
-    for (int py = max(h + 1 - lag, 0); py < h; ++py) finalize(py);
-}
-
-// Column prefix carries for the segmented mode pass: for every column x, bin
-// lane-group and segment k, the exclusive prefix sum of H over the rows
-// before j0(k) = max(0, k*seg - lag) (integers: exact in any order).
-template <int VPL>
-__global__ void k_refine_carry(const uint8_t* __restrict__ hcnt, int w, int h, int seg, int nseg, int lag,
-                               unsigned* __restrict__ carry /* [x][nseg][32 lanes] packed u16 x VPL in u32s */) {
-    const int lane = threadIdx.x & 31;
-    const int x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (x >= w) return;
-    const int nbp = 32 * VPL;
-    const size_t rowstride = static_cast<size_t>(w) * nbp;
-    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
-    unsigned acc[VPL];
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) acc[j] = 0;
-    int y = 0;
-    for (int k = 0; k < nseg; ++k) {
-        const int j0 = max(0, k * seg - lag);
-        for (; y < j0; ++y) {
-            const uint8_t* hp = src + y * rowstride;
-#pragma unroll
-            for (int j = 0; j < VPL; ++j) acc[j] += hp[j];
-        }
-        unsigned* dst = carry + ((static_cast<size_t>(x) * nseg + k) * 32 + lane) * VPL;
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) dst[j] = acc[j];
-    }
-}
+// Counts are integers, so any summation order is exact. k_refine_hscatter
+// builds H densely; k_refine_segsum sums it per (column, row segment); the
+// mode pass walks each segment of each column with a prefix ring seeded from
+// the segment sums and takes the mode (max count, smallest bin on ties).
+// Cost O(N * bins) instead of O(N * region) -- regions reach 35x35.
 
 // Segmented mode pass: warp per (column x, row segment k); the prefix ring is
 // seeded from the carry, so segments run in parallel. H rows are prefetched
@@ -1096,6 +966,209 @@ __global__ void k_refine_vmode2(const float* __restrict__ cur, const uint8_t* __
     for (int py = max(yend + 1 - lag, out0); py < out1; ++py) {
         const size_t i = static_cast<size_t>(py) * w + x;
         finalize(py, cur[i], U[i], D[i]);
+    }
+}
+
+// Packed segmented mode pass (the production path): as k_refine_vmode2, but
+// two u16 bin prefixes share one u32 (a column prefix never exceeds
+// h * (2*l1+1) < 65536, so the halves never carry into each other and the
+// packed difference of two prefixes is the pair of exact counts), one
+// vector shared-memory access per slot, and the (count, -bin) argmax and the
+// region total as two warp REDUX ops.
+template <int VPL>
+__global__ void k_refine_vmode3(const float* __restrict__ cur, const uint8_t* __restrict__ hcnt, int w, int h,
+                                const uint8_t* __restrict__ U, const uint8_t* __restrict__ D, int lag, int ring_n,
+                                int seg, int nseg, const unsigned* __restrict__ carry, float* __restrict__ next) {
+    static_assert(VPL == 2 || VPL == 4 || VPL == 8, "packed pairs");
+    constexpr int W2 = VPL / 2;
+    extern __shared__ uint32_t ringw[];  // per warp: [ring_n][32 lanes][W2]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+    const int x = gw / nseg, k = gw - x * nseg;
+    if (x >= w) return;
+    const int nbp = 32 * VPL;
+    uint32_t* rg = ringw + static_cast<size_t>(warp) * ring_n * 32 * W2 + lane * W2;
+    auto slot_ptr = [&](int slot) { return rg + slot * 32 * W2; };
+    auto load_slot = [&](int slot, uint32_t (&o)[W2]) {
+        const uint32_t* p = slot_ptr(slot);
+        if constexpr (W2 == 1) {
+            o[0] = p[0];
+        } else if constexpr (W2 == 2) {
+            uint2 v = *reinterpret_cast<const uint2*>(p);
+            o[0] = v.x;
+            o[1] = v.y;
+        } else {
+            uint4 v = *reinterpret_cast<const uint4*>(p);
+            o[0] = v.x;
+            o[1] = v.y;
+            o[2] = v.z;
+            o[3] = v.w;
+        }
+    };
+    auto store_slot = [&](int slot, const uint32_t (&o)[W2]) {
+        uint32_t* p = slot_ptr(slot);
+        if constexpr (W2 == 1) {
+            p[0] = o[0];
+        } else if constexpr (W2 == 2) {
+            *reinterpret_cast<uint2*>(p) = make_uint2(o[0], o[1]);
+        } else {
+            *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    };
+    const int j0 = max(0, k * seg - lag);
+    const int out0 = k * seg, out1 = min(h, (k + 1) * seg);
+    const int yend = min(h, out1 + lag);
+    uint32_t C[W2];
+    {
+        unsigned cs[VPL];
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) cs[j] = 0;
+        for (int kk = 0; kk < k; ++kk) {  // exclusive prefix of the segment sums
+            const unsigned* cin = carry + ((static_cast<size_t>(x) * nseg + kk) * 32 + lane) * VPL;
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) cs[j] += cin[j];
+        }
+#pragma unroll
+        for (int q = 0; q < W2; ++q) C[q] = (cs[2 * q] & 0xffffu) | (cs[2 * q + 1] << 16);
+    }
+    int s1 = 0;  // slot of C after row y (prefix through row y): starts as the prefix before j0
+    store_slot(0, C);
+    auto finalize = [&](int sa, int sb, float center, int py) {
+        uint32_t A[W2], B[W2];
+        load_slot(sa, A);
+        load_slot(sb, B);
+        uint32_t key = 0;
+        int tot = 0;
+#pragma unroll
+        for (int q = 0; q < W2; ++q) {
+            const uint32_t dlt = B[q] - A[q];
+            const uint32_t c0 = dlt & 0xffffu, c1 = dlt >> 16;
+            const uint32_t b0 = static_cast<uint32_t>(lane * VPL + 2 * q);
+            tot += static_cast<int>(c0 + c1);
+            const uint32_t k0 = c0 ? (c0 << 16) | (0xffffu - b0) : 0u;
+            const uint32_t k1 = c1 ? (c1 << 16) | (0xffffu - b0 - 1u) : 0u;
+            key = max(key, max(k0, k1));
+        }
+        const uint32_t wkey = __reduce_max_sync(0xffffffffu, key);
+        const int total = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(tot)));
+        if (lane == 0) {
+            float o = center;  // removed outliers stay removed
+            if (isfinite(center)) {
+                const int best_c = static_cast<int>(wkey >> 16);
+                const int best_b = static_cast<int>(0xffffu - (wkey & 0xffffu));
+                o = (best_c == 1 && total >= 4) ? __int_as_float(0x7fc00000) : static_cast<float>(best_b);
+            }
+            next[static_cast<size_t>(py) * w + x] = o;
+        }
+    };
+    // ring slot of the prefix through row yy (C[yy+1] in prefix terms) relative
+    // to s1 = slot of the prefix through row y: slot(y) - (y - yy)
+    auto rel = [&](int base_slot, int back) {
+        int sl = base_slot - back;
+        return sl < 0 ? sl + ring_n : sl;
+    };
+    const size_t rowstride = static_cast<size_t>(w) * nbp;
+    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
+    auto load_h = [&](int y, uint32_t (&o)[W2]) {
+        if constexpr (VPL == 2) {
+            const uint32_t v = *reinterpret_cast<const unsigned short*>(src + y * rowstride);
+            o[0] = __byte_perm(v, 0u, 0x4140);
+        } else if constexpr (VPL == 4) {
+            const uint32_t v = *reinterpret_cast<const uint32_t*>(src + y * rowstride);
+            o[0] = __byte_perm(v, 0u, 0x4140);
+            o[1] = __byte_perm(v, 0u, 0x4342);
+        } else {
+            const uint2 v = *reinterpret_cast<const uint2*>(src + y * rowstride);
+            o[0] = __byte_perm(v.x, 0u, 0x4140);
+            o[1] = __byte_perm(v.x, 0u, 0x4342);
+            o[2] = __byte_perm(v.y, 0u, 0x4140);
+            o[3] = __byte_perm(v.y, 0u, 0x4342);
+        }
+    };
+    constexpr int kPF = 8;
+    uint32_t pf[kPF][W2];
+    float cq[kPF];
+    uint32_t aq[kPF];  // up | down << 8 of the row finalised at this step
+    auto load_meta = [&](int y, float& c, uint32_t& a) {
+        const int py = y + 1 - lag;
+        c = 0.0f;
+        a = 0u;
+        if (py >= out0 && py < out1) {
+            const size_t i = static_cast<size_t>(py) * w + x;
+            c = cur[i];
+            a = U[i] | (static_cast<uint32_t>(D[i]) << 8);
+        }
+    };
+#pragma unroll
+    for (int q = 0; q < kPF; ++q) {
+        if (j0 + q < yend) {
+            load_h(j0 + q, pf[q]);
+        } else {
+#pragma unroll
+            for (int t = 0; t < W2; ++t) pf[q][t] = 0u;
+        }
+        load_meta(j0 + q, cq[q], aq[q]);
+    }
+    for (int y0 = j0; y0 < yend; y0 += kPF) {
+        uint32_t nx[kPF][W2];
+        float nc[kPF];
+        uint32_t na[kPF];
+#pragma unroll
+        for (int q = 0; q < kPF; ++q) {
+            const int y = y0 + kPF + q;
+            if (y < yend) {
+                load_h(y, nx[q]);
+            } else {
+#pragma unroll
+                for (int t = 0; t < W2; ++t) nx[q][t] = 0u;
+            }
+            load_meta(y, nc[q], na[q]);
+        }
+        // prefixes of the whole chunk, then its outputs
+        const int sb0 = s1;
+#pragma unroll
+        for (int q = 0; q < kPF; ++q) {
+            if (y0 + q < yend) {
+#pragma unroll
+                for (int t = 0; t < W2; ++t) C[t] += pf[q][t];
+                s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
+                store_slot(s1, C);
+            }
+        }
+        __syncwarp();
+        int sq = sb0;
+#pragma unroll
+        for (int q = 0; q < kPF; ++q) {
+            const int y = y0 + q;
+            if (y < yend) {
+                sq = (sq + 1 == ring_n) ? 0 : sq + 1;  // slot of the prefix through row y
+                const int py = y + 1 - lag;
+                if (py >= out0 && py < out1) {
+                    const int up = aq[q] & 255u, dn = (aq[q] >> 8) & 255u;
+                    // counts over rows [py - up, py + dn] = P(py + dn) - P(py - up - 1)
+                    const int sb = rel(sq, y - (py + dn));
+                    const int sa = rel(sq, y - (py - up - 1));
+                    finalize(sa, sb, cq[q], py);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kPF; ++q) {
+#pragma unroll
+            for (int t = 0; t < W2; ++t) pf[q][t] = nx[q][t];
+            cq[q] = nc[q];
+            aq[q] = na[q];
+        }
+    }
+    // rows whose window reaches the image bottom; s1 = slot of the prefix through row yend - 1
+    for (int py = max(yend + 1 - lag, out0); py < out1; ++py) {
+        const size_t i = static_cast<size_t>(py) * w + x;
+        const int up = U[i], dn = D[i];
+        const int last = yend - 1;
+        const int sb = rel(s1, last - (py + dn));
+        const int sa = rel(s1, last - (py - up - 1));
+        finalize(sa, sb, cur[i], py);
     }
 }
 
@@ -1389,7 +1462,7 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     const float* src = disp;
     const unsigned blocks = static_cast<unsigned>(std::min<size_t>(blocks_for(n, warps), 148 * 16));
     // exact integer cross-aggregation of one-hot bins (preferred, O(N*bins))
-    const int nbp = cap <= 32 ? 32 : cap <= 64 ? 64 : cap <= 128 ? 128 : cap <= 256 ? 256 : 0;
+    const int nbp = cap <= 64 ? 64 : cap <= 128 ? 128 : cap <= 256 ? 256 : 0;
     uint8_t* hcnt = nbp ? static_cast<uint8_t*>(scratch(ctx, S_HSUM, n * nbp)) : nullptr;
     const int lag = max_arm + 1, ring = ring_size(max_arm);
     const int vwarps = 4;
@@ -1397,11 +1470,9 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     const size_t hsmem = static_cast<size_t>(nbp) * ((w + 31) / 32) * sizeof(unsigned);
     static bool attr_v = false;
     if (!attr_v) {
-        cudaFuncSetAttribute(k_refine_hcount, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode3<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_refine_vmode3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(k_refine_vmode2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(k_refine_vmode2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(k_refine_vmode2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -1409,6 +1480,10 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
         attr_v = true;
     }
     const bool aggregated = nbp && vsmem <= 200 * 1024 && hsmem <= 200 * 1024;
+    // packed u16 pairs: every column prefix stays below 65536
+    const bool packed = aggregated && nbp >= 64 && static_cast<long>(h) * (2 * max_arm + 1) < 65536;
+    const int ring3 = 8 + 2 * max_arm + 2;
+    const size_t vsmem3 = static_cast<size_t>(vwarps) * ring3 * 32 * (nbp / 64) * sizeof(uint32_t);
     const bool per_thread = cap <= 256;
     const size_t smem_t = static_cast<size_t>(cap) * kHistThreads * sizeof(unsigned short);
     static bool attr_t = false;
@@ -1427,6 +1502,29 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
             const int seg = 32, nseg = (h + seg - 1) / seg;
             unsigned* carry = static_cast<unsigned*>(scratch(ctx, S_TMP1, static_cast<size_t>(w) * nseg * nbp * 4));
             dim3 vb(32 * vwarps), vg((w * nseg + vwarps - 1) / vwarps);
+            if (packed) {
+                switch (nbp / 32) {
+                    case 2:
+                        k_refine_segsum<2><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                        k_refine_vmode3<2><<<vg, vb, vsmem3, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring3, seg,
+                                                                            nseg, carry, dst);
+                        break;
+                    case 4:
+                        k_refine_segsum<4><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                        k_refine_vmode3<4><<<vg, vb, vsmem3, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring3, seg,
+                                                                            nseg, carry, dst);
+                        break;
+                    default:
+                        k_refine_segsum<8><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                        k_refine_vmode3<8><<<vg, vb, vsmem3, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring3, seg,
+                                                                            nseg, carry, dst);
+                        break;
+                }
+                launched(ctx, "k_refine_segsum");
+                launched(ctx, "k_refine_vmode3");
+                src = dst;
+                continue;
+            }
             switch (nbp / 32) {
                 case 1:
                     k_refine_segsum<1><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
@@ -1445,8 +1543,8 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
                     k_refine_vmode2<8><<<vg, vb, vsmem, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring - 1, seg, nseg, carry, dst);
                     break;
             }
-            launched(ctx, "k_refine_carry");
-            launched(ctx, "k_refine_vmode");
+            launched(ctx, "k_refine_segsum");
+            launched(ctx, "k_refine_vmode2");
         } else if (per_thread) {
             k_hist_refine_thread<<<blocks_t, kHistThreads, smem_t, ctx->stream>>>(src, w, h, l, r, u, d, bmax, cap, dst);
             launched(ctx, "k_hist_refine_thread");
