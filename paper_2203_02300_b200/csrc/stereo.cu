@@ -1020,14 +1020,24 @@ __global__ void k_refine_vmode3(const float* __restrict__ cur, const uint8_t* __
     const int yend = min(h, out1 + lag);
     uint32_t C[W2];
     {
+        // exclusive prefix of the segment sums: the first 8 loads issue together
         unsigned cs[VPL];
 #pragma unroll
         for (int j = 0; j < VPL; ++j) cs[j] = 0;
-        for (int kk = 0; kk < k; ++kk) {  // exclusive prefix of the segment sums
-            const unsigned* cin = carry + ((static_cast<size_t>(x) * nseg + kk) * 32 + lane) * VPL;
+        const unsigned* cin = carry + (static_cast<size_t>(x) * nseg * 32 + lane) * VPL;
+        constexpr int kU = 8;
+        unsigned part[kU][VPL];
 #pragma unroll
-            for (int j = 0; j < VPL; ++j) cs[j] += cin[j];
-        }
+        for (int kk = 0; kk < kU; ++kk)
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) part[kk][j] = kk < k ? cin[kk * 32 * VPL + j] : 0u;
+#pragma unroll
+        for (int kk = 0; kk < kU; ++kk)
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) cs[j] += part[kk][j];
+        for (int kk = kU; kk < k; ++kk)
+#pragma unroll
+            for (int j = 0; j < VPL; ++j) cs[j] += cin[kk * 32 * VPL + j];
 #pragma unroll
         for (int q = 0; q < W2; ++q) C[q] = (cs[2 * q] & 0xffffu) | (cs[2 * q + 1] << 16);
     }
@@ -1068,69 +1078,100 @@ __global__ void k_refine_vmode3(const float* __restrict__ cur, const uint8_t* __
         return sl < 0 ? sl + ring_n : sl;
     };
     const size_t rowstride = static_cast<size_t>(w) * nbp;
-    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
-    auto load_h = [&](int y, uint32_t (&o)[W2]) {
+    // raw H words are kept as loaded (VPL bytes per lane) and unpacked into
+    // u16 pairs only when consumed, so the prefetch really stays in flight
+    constexpr int RW = (VPL + 3) / 4;  // raw u32 words per row (VPL=2 uses the low half)
+    auto load_raw = [&](const uint8_t* p, uint32_t (&o)[RW]) {
         if constexpr (VPL == 2) {
-            const uint32_t v = *reinterpret_cast<const unsigned short*>(src + y * rowstride);
-            o[0] = __byte_perm(v, 0u, 0x4140);
+            o[0] = *reinterpret_cast<const unsigned short*>(p);
         } else if constexpr (VPL == 4) {
-            const uint32_t v = *reinterpret_cast<const uint32_t*>(src + y * rowstride);
-            o[0] = __byte_perm(v, 0u, 0x4140);
-            o[1] = __byte_perm(v, 0u, 0x4342);
+            o[0] = *reinterpret_cast<const uint32_t*>(p);
         } else {
-            const uint2 v = *reinterpret_cast<const uint2*>(src + y * rowstride);
-            o[0] = __byte_perm(v.x, 0u, 0x4140);
-            o[1] = __byte_perm(v.x, 0u, 0x4342);
-            o[2] = __byte_perm(v.y, 0u, 0x4140);
-            o[3] = __byte_perm(v.y, 0u, 0x4342);
+            const uint2 v = *reinterpret_cast<const uint2*>(p);
+            o[0] = v.x;
+            o[1] = v.y;
         }
     };
+    auto unpack = [&](const uint32_t (&r)[RW], uint32_t (&o)[W2]) {
+#pragma unroll
+        for (int q = 0; q < RW; ++q) {
+            o[2 * q] = __byte_perm(r[q], 0u, 0x4140);
+            if (2 * q + 1 < W2) o[2 * q + 1] = __byte_perm(r[q], 0u, 0x4342);
+        }
+    };
+    // hp: next H row to load
+    const uint8_t* hp = hcnt + static_cast<size_t>(j0) * rowstride + static_cast<size_t>(x) * nbp + lane * VPL;
     constexpr int kPF = 8;
-    uint32_t pf[kPF][W2];
+    uint32_t pf[kPF][RW];
     float cq[kPF];
-    uint32_t aq[kPF];  // up | down << 8 of the row finalised at this step
-    auto load_meta = [&](int y, float& c, uint32_t& a) {
+    uint32_t uq[kPF], dq[kPF];  // arms of the row finalised at this step
+    auto load_meta = [&](int y, float& c, uint32_t& a, uint32_t& b) {
         const int py = y + 1 - lag;
         c = 0.0f;
-        a = 0u;
+        a = b = 0u;
         if (py >= out0 && py < out1) {
             const size_t i = static_cast<size_t>(py) * w + x;
             c = cur[i];
-            a = U[i] | (static_cast<uint32_t>(D[i]) << 8);
+            a = U[i];
+            b = D[i];
         }
     };
 #pragma unroll
     for (int q = 0; q < kPF; ++q) {
         if (j0 + q < yend) {
-            load_h(j0 + q, pf[q]);
+            load_raw(hp, pf[q]);
         } else {
 #pragma unroll
-            for (int t = 0; t < W2; ++t) pf[q][t] = 0u;
+            for (int t = 0; t < RW; ++t) pf[q][t] = 0u;
         }
-        load_meta(j0 + q, cq[q], aq[q]);
+        hp += rowstride;
+        load_meta(j0 + q, cq[q], uq[q], dq[q]);
     }
     for (int y0 = j0; y0 < yend; y0 += kPF) {
-        uint32_t nx[kPF][W2];
+        uint32_t nx[kPF][RW];
         float nc[kPF];
-        uint32_t na[kPF];
+        uint32_t nu[kPF], nd[kPF];
+        // chunk fully inside [j0, yend) with every row finalised: no per-row checks
+        const bool fast = y0 + 2 * kPF <= yend && y0 + kPF + 1 - lag >= out0 && y0 + 2 * kPF - lag < out1;
+        if (fast) {
+            const size_t mi = static_cast<size_t>(y0 + kPF + 1 - lag) * w + x;
+            const float* cp = cur + mi;
+            const uint8_t* up = U + mi;
+            const uint8_t* dp = D + mi;
 #pragma unroll
-        for (int q = 0; q < kPF; ++q) {
-            const int y = y0 + kPF + q;
-            if (y < yend) {
-                load_h(y, nx[q]);
-            } else {
-#pragma unroll
-                for (int t = 0; t < W2; ++t) nx[q][t] = 0u;
+            for (int q = 0; q < kPF; ++q) {
+                load_raw(hp, nx[q]);
+                hp += rowstride;
+                nc[q] = *cp;
+                nu[q] = *up;
+                nd[q] = *dp;
+                cp += w;
+                up += w;
+                dp += w;
             }
-            load_meta(y, nc[q], na[q]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kPF; ++q) {
+                const int y = y0 + kPF + q;
+                if (y < yend) {
+                    load_raw(hp, nx[q]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < RW; ++t) nx[q][t] = 0u;
+                }
+                hp += rowstride;
+                load_meta(y, nc[q], nu[q], nd[q]);
+            }
         }
         // prefixes of the whole chunk, then its outputs
         const int sb0 = s1;
 #pragma unroll
         for (int q = 0; q < kPF; ++q) {
             if (y0 + q < yend) {
+                uint32_t hv[W2];
+                unpack(pf[q], hv);
 #pragma unroll
-                for (int t = 0; t < W2; ++t) C[t] += pf[q][t];
+                for (int t = 0; t < W2; ++t) C[t] += hv[t];
                 s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
                 store_slot(s1, C);
             }
@@ -1144,10 +1185,9 @@ __global__ void k_refine_vmode3(const float* __restrict__ cur, const uint8_t* __
                 sq = (sq + 1 == ring_n) ? 0 : sq + 1;  // slot of the prefix through row y
                 const int py = y + 1 - lag;
                 if (py >= out0 && py < out1) {
-                    const int up = aq[q] & 255u, dn = (aq[q] >> 8) & 255u;
                     // counts over rows [py - up, py + dn] = P(py + dn) - P(py - up - 1)
-                    const int sb = rel(sq, y - (py + dn));
-                    const int sa = rel(sq, y - (py - up - 1));
+                    const int sb = rel(sq, lag - 1 - static_cast<int>(dq[q]));
+                    const int sa = rel(sq, lag + static_cast<int>(uq[q]));
                     finalize(sa, sb, cq[q], py);
                 }
             }
@@ -1156,9 +1196,10 @@ __global__ void k_refine_vmode3(const float* __restrict__ cur, const uint8_t* __
 #pragma unroll
         for (int q = 0; q < kPF; ++q) {
 #pragma unroll
-            for (int t = 0; t < W2; ++t) pf[q][t] = nx[q][t];
+            for (int t = 0; t < RW; ++t) pf[q][t] = nx[q][t];
             cq[q] = nc[q];
-            aq[q] = na[q];
+            uq[q] = nu[q];
+            dq[q] = nd[q];
         }
     }
     // rows whose window reaches the image bottom; s1 = slot of the prefix through row yend - 1
@@ -1233,6 +1274,37 @@ __global__ void k_refine_segsum(const uint8_t* __restrict__ hcnt, int w, int h, 
     unsigned* dst = segsum + ((static_cast<size_t>(x) * nseg + k) * 32 + lane) * VPL;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) dst[j] = acc[j];
+}
+
+// k_refine_segsum with the rows of one (column, segment) split over the 4
+// warps of a block (integer partial sums: exact in any order).
+template <int VPL>
+__global__ void __launch_bounds__(128) k_refine_segsum4(const uint8_t* __restrict__ hcnt, int w, int h, int seg,
+                                                        int nseg, int lag, unsigned* __restrict__ segsum) {
+    __shared__ unsigned part[4][32 * VPL];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int x = blockIdx.x / nseg, k = blockIdx.x - x * nseg;
+    const int nbp = 32 * VPL;
+    const int y0 = max(0, k * seg - lag), y1 = (k + 1 < nseg) ? max(0, (k + 1) * seg - lag) : h;
+    const size_t rowstride = static_cast<size_t>(w) * nbp;
+    const uint8_t* src = hcnt + static_cast<size_t>(x) * nbp + lane * VPL;
+    unsigned acc[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) acc[j] = 0;
+#pragma unroll 4
+    for (int y = y0 + wp; y < y1; y += 4)
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) acc[j] += src[y * rowstride + j];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) part[wp][lane * VPL + j] = acc[j];
+    __syncthreads();
+    if (wp == 0) {
+        unsigned* dst = segsum + ((static_cast<size_t>(x) * nseg + k) * 32 + lane) * VPL;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j)
+            dst[j] = part[0][lane * VPL + j] + part[1][lane * VPL + j] + part[2][lane * VPL + j] +
+                     part[3][lane * VPL + j];
+    }
 }
 
 // -------------------------------------------------------- sparse depth -----
@@ -1499,28 +1571,28 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
                                 kHcThreads, static_cast<size_t>(nbp) * kHcThreads, ctx->stream>>>(src, w, h, l, r,
                                                                                                   nbp, hcnt);
             launched(ctx, "k_refine_hscatter");
-            const int seg = 32, nseg = (h + seg - 1) / seg;
+            const int seg = packed ? 64 : 32, nseg = (h + seg - 1) / seg;
             unsigned* carry = static_cast<unsigned*>(scratch(ctx, S_TMP1, static_cast<size_t>(w) * nseg * nbp * 4));
             dim3 vb(32 * vwarps), vg((w * nseg + vwarps - 1) / vwarps);
             if (packed) {
                 switch (nbp / 32) {
                     case 2:
-                        k_refine_segsum<2><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                        k_refine_segsum4<2><<<w * nseg, 128, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
                         k_refine_vmode3<2><<<vg, vb, vsmem3, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring3, seg,
                                                                             nseg, carry, dst);
                         break;
                     case 4:
-                        k_refine_segsum<4><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                        k_refine_segsum4<4><<<w * nseg, 128, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
                         k_refine_vmode3<4><<<vg, vb, vsmem3, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring3, seg,
                                                                             nseg, carry, dst);
                         break;
                     default:
-                        k_refine_segsum<8><<<vg, vb, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
+                        k_refine_segsum4<8><<<w * nseg, 128, 0, ctx->stream>>>(hcnt, w, h, seg, nseg, lag, carry);
                         k_refine_vmode3<8><<<vg, vb, vsmem3, ctx->stream>>>(src, hcnt, w, h, u, d, lag, ring3, seg,
                                                                             nseg, carry, dst);
                         break;
                 }
-                launched(ctx, "k_refine_segsum");
+                launched(ctx, "k_refine_segsum4");
                 launched(ctx, "k_refine_vmode3");
                 src = dst;
                 continue;
