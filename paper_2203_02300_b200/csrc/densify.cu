@@ -874,6 +874,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
     }
 }
 
+}  // namespace
+}  // namespace dco_gpu
+
+#include "pcg_tmem.cuh"
+
+namespace dco_gpu {
+namespace {
+
 inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
 
 int g_pcg_blocks = 0;
@@ -884,6 +892,19 @@ int g_sms = 0;
 typedef void (*OnchipKernel)(CGArgs, int, GridBar*);
 constexpr int kOnchipThreadsUsed = 1024;
 constexpr int kOnchipSmemMax = 222 * 1024;  // + 2.6 KB static reduction scratch <= 227 KB
+OnchipKernel tmem_for(int ept) {
+    switch (ept) {
+        case 1: return k_pcg_tmem<1>;
+        case 2: return k_pcg_tmem<2>;
+        case 3: return k_pcg_tmem<3>;
+        case 4: return k_pcg_tmem<4>;
+        case 5: return k_pcg_tmem<5>;
+        case 6: return k_pcg_tmem<6>;
+        case 7: return k_pcg_tmem<7>;
+        case 8: return k_pcg_tmem<8>;
+        default: return nullptr;
+    }
+}
 OnchipKernel onchip_for(int threads, int ept) {
     if (threads != 1024) return nullptr;
     switch (ept) {
@@ -1034,14 +1055,19 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     const int threads = kOnchipThreadsUsed;
     const int ept = (chunk + threads - 1) / threads;
     const size_t smem = (static_cast<size_t>(chunk) * 4 + 2 * static_cast<size_t>(w)) * sizeof(double);
-    OnchipKernel kern = onchip_for(threads, ept);
+    // registers + TMEM + shared memory (pcg_tmem.cuh); DCO_PCG_NO_TMEM=1 selects
+    // the registers + shared-memory variant
+    static const bool no_tmem = getenv("DCO_PCG_NO_TMEM") != nullptr;
+    OnchipKernel kern = no_tmem ? onchip_for(threads, ept) : tmem_for(ept);
     if (kern && smem <= kOnchipSmemMax && sms <= 1024) {
-        static bool attr[17] = {};
-        if (!attr[ept]) {
+        // dynamic shared memory: exactly this launch's need (static scratch
+        // comes on top, 227 KB per CTA in total)
+        static int attr[2][17] = {};
+        if (attr[no_tmem][ept] < static_cast<int>(smem)) {
             cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kOnchipSmemMax),
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "smem attr");
-            attr[ept] = true;
+            attr[no_tmem][ept] = static_cast<int>(smem);
         }
         int chunk_arg = chunk;
         GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
@@ -1049,7 +1075,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         void* params[] = {&a, &chunk_arg, &bar};
         launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(threads),
                                       params, smem);
-        launched(ctx, "k_pcg_onchip");
+        launched(ctx, no_tmem ? "k_pcg_onchip" : "k_pcg_tmem");
         return;
     }
     void* params[] = {&a};

@@ -28,9 +28,12 @@ lib.dco_debug_pcg_stamps(buf, LEN)
 g = np.array(buf[1280:]).reshape(64, 1024, 3)[:, :NB, :].astype(np.float64)
 a = np.array(buf[:640]).reshape(64, 10)
 b = np.array(buf[640:1280]).reshape(64, 10)
-names = ["A (MR tail + SpMV) work", "A barrier-reduce", "B work", "B barrier-reduce"]
+# stamps: 0 loop head, 3 after halo, 4 after P1, 5 after CTA barrier, 1 after P2, 2 after grid barrier
+order = [0, 3, 4, 5, 1, 2]
+names = ["halo fill", "P1 (update)", "CTA barrier", "P2 (SpMV + sums)", "grid barrier-reduce"]
 for tag, m in (("block0", a), ("last", b)):
-    d = np.diff(m[5:40, :5], axis=1).mean(axis=0)
+    mm = m[5:40][:, order]
+    d = np.diff(mm, axis=1).mean(axis=0)
     tot = (m[6:40, 0] - m[5:39, 0]).mean()
     print(tag, "cycles/iter %.0f" % tot)
     for n, v in zip(names, d):
