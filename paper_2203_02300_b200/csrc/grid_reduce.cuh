@@ -8,8 +8,9 @@
 //     reduces P values with P/2 + P/4 + ... + 1 shuffles (not 5 K).
 //  2. block level: warp 0 sums the per-warp rows in shared memory and writes
 //     the block's row into a transposed partial table partials[k][block].
-//  3. arrival on a monotonic counter (never reset inside a launch: barrier g
-//     completes at count == nb * (g + 1)); release / acquire at gpu scope.
+//  3. arrival on monotonic counters (never reset inside a launch: barrier g
+//     completes when every stripe's count reaches members * (g + 1));
+//     release / acquire at gpu scope.
 //     Two partial tables alternate, so a block one barrier ahead never
 //     overwrites a row still being read.
 //  4. every block sums all rows itself, value k on warp k, coalesced loads.
@@ -17,9 +18,11 @@
 
 namespace dco_gpu {
 
+// Arrival counters striped over kGridBarStripes cache lines: same-address
+// atomics serialise at their L2 slice, so block b arrives on stripe b % S.
+constexpr int kGridBarStripes = 8;
 struct GridBar {
-    unsigned count;
-    unsigned pad[31];
+    unsigned count[kGridBarStripes][32];  // one 128 B line per stripe
 };
 
 template <int K>
@@ -64,7 +67,9 @@ __device__ __forceinline__ int grid_reduce_index(int lane) {
 }
 
 // sm: >= 32 * 16 doubles of shared scratch. partials: 2 * 16 * gridDim.x doubles.
-template <int K>
+// kTailSync = false skips the closing CTA barrier: the caller guarantees a
+// __syncthreads() before sm is written again.
+template <int K, bool kTailSync = true>
 __device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, double* partials, unsigned& gen,
                                                double* sm, double (&res)[K]) {
     constexpr int P = ReducePad<K>::P;
@@ -92,18 +97,25 @@ __device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, dou
         for (int off = 16; off >= P; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane < K) __stcg(table + static_cast<size_t>(lane) * nb + blockIdx.x, s);
         __syncwarp();
-        // 3. arrive, wait for everyone
-        if (lane == 0) {
-            const unsigned target = static_cast<unsigned>(nb) * (gen + 1u);
+        // 3. arrive on this block's stripe; lanes 0..S-1 each wait for one stripe
+        if (lane == 0)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&bar->count[blockIdx.x % kGridBarStripes][0])
+                         : "memory");
+        if (lane < kGridBarStripes) {
+            const unsigned members = static_cast<unsigned>((nb - lane + kGridBarStripes - 1) / kGridBarStripes);
+            const unsigned target = members * (gen + 1u);
             unsigned c;
-            asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(c) : "l"(&bar->count) : "memory");
-            ++c;
-            while (c < target) asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(c) : "l"(&bar->count) : "memory");
+            do {
+                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(c) : "l"(&bar->count[lane][0]) : "memory");
+            } while (c < target);
         }
+        __syncwarp();
     }
     __syncthreads();
     // 4. value k on warp k: coalesced loads of row k, fixed-order tree
-    double* sres = sm;  // step 2's reads finished before the barrier
+    // step 2's reads finished before the barrier; the top 16 slots stay clear
+    // of a following K <= 2 step 1 when kTailSync = false
+    double* sres = sm + 32 * 16 - 16;
     if (warp < K) {
         double s = 0.0;
         for (int b = lane; b < nb; b += 32) s += __ldcg(table + static_cast<size_t>(warp) * nb + b);
@@ -115,7 +127,7 @@ __device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, dou
 #pragma unroll
     for (int k = 0; k < K; ++k) res[k] = sres[k];
     ++gen;
-    __syncthreads();  // sm reused by the next reduction
+    if (kTailSync) __syncthreads();  // sm reused by the next reduction
 }
 
 }  // namespace dco_gpu

@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
             }
             STAMP(1)
             double res[10];
-            barrier_reduce<10>(v, bar, a.part, gen, sm, res);
+            barrier_reduce<10, false>(v, bar, a.part, gen, sm, res);  // CTA barrier before P2 guards sm
             STAMP(2)
             if (iter > 0) {
                 snorm = sqrt(res[1]);
