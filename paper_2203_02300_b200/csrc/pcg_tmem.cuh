@@ -16,6 +16,8 @@
 // columns above 8*EPT, the x of as many slots as fit.
 #pragma once
 
+#include <type_traits>
+
 namespace dco_gpu {
 namespace {
 
@@ -53,6 +55,26 @@ __device__ __forceinline__ void tm_st2(uint32_t a, const uint32_t (&v)[2]) {
 }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// explicit 32-bit shared-window accesses: base register + immediate, so the
+// compiler neither rematerialises the window base per access nor spends a
+// register per array
+template <int IMM>
+__device__ __forceinline__ double lds(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(IMM) : "memory");
+    return v;
+}
+template <int IMM>
+__device__ __forceinline__ void sts(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(IMM), "d"(v) : "memory");
+}
+template <int K, int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (K < N) {
+        f(std::integral_constant<int, K>{});
+        static_for<K + 1, N>(f);
+    }
+}
 __device__ __forceinline__ double u2d(uint32_t lo, uint32_t hi) {
     return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
 }
@@ -81,6 +103,12 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
     double* s_ch = sx + 2 * w + chunk + t;
     double* s_cv = sx + 2 * w + 2 * chunk + t;
     double* s_pr = sx + 2 * w + 3 * chunk + t;
+    // shared-window byte addresses of this thread's slot 0 (loop accesses)
+    const uint32_t aP = static_cast<uint32_t>(__cvta_generic_to_shared(s_p));
+    const uint32_t aCH = static_cast<uint32_t>(__cvta_generic_to_shared(s_ch));
+    const uint32_t aCV = static_cast<uint32_t>(__cvta_generic_to_shared(s_cv));
+    const uint32_t aPR = static_cast<uint32_t>(__cvta_generic_to_shared(s_pr));
+    const uint32_t wb = 8u * static_cast<uint32_t>(w);
     unsigned gen = 0;
     double r[EPT], x[EPT];
     unsigned pub = 0;  // bit k: slot k lies in a row other blocks read as halo
@@ -249,8 +277,8 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
 #pragma unroll
             for (int c = 0; c < 10; ++c) v[c] = 0.0;
             tm_wait_st();  // last phase's q / xs / rs stores have landed
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
+            static_for<0, EPT>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
                 uint32_t c4[4], c2[2], cx[2];
                 tm_ld4(tm + 8 * k, c4);      // q, xs
                 tm_ld2(tm + 8 * k + 4, c2);  // rs
@@ -262,15 +290,15 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
                 double xk = k < XT ? u2d(cx[0], cx[1]) : x[k];
                 if (DCO_OK(k)) {
                     const int o = KO(k);
-                    double pk = s_p[o];
+                    double pk = lds<8 * KO(k)>(aP);
                     double ri = r[k];
-                    const double pr = s_pr[o];
+                    const double pr = lds<8 * KO(k)>(aPR);
                     if (iter) {
                         xk = __fma_rn(alpha, pk, xk);
                         ri = __fma_rn(-alpha, qk, ri);
                         pk = __fma_rn(beta, pk, pr * ri);
                         r[k] = ri;
-                        s_p[o] = pk;
+                        sts<8 * KO(k)>(aP, pk);
                         if (eta > 0.0) {
                             rsi = __fma_rn(eta, ri - rsi, rsi);
                             xsi = __fma_rn(eta, xk - xsi, xsi);
@@ -298,7 +326,7 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
                     d2u(rsi, s4[2], s4[3]);
                     tm_st4(tm + 8 * k + 2, s4);
                 }
-            }
+            });
             // P1 sums -> per-warp partials in shared memory (frees registers for P2)
 #pragma unroll
             for (int c = 1; c <= 4; ++c) {
@@ -315,8 +343,8 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
             uint32_t cur4[4];
             tm_ld4(tm + 4, cur4);  // rs, diag of slot 0
             tm_wait_ld();
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
+            static_for<0, EPT>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
                 uint32_t nxt4[4];
                 if (k + 1 < EPT) tm_ld4(tm + 8 * (k + 1) + 4, nxt4);  // in flight during slot k
                 const double rsi = u2d(cur4[0], cur4[1]);
@@ -325,26 +353,26 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
                 if (DCO_OK(k)) {
                     const int o = KO(k);
                     const int l = t + o;
-                    const double pk = s_p[o];
+                    const double pk = lds<8 * KO(k)>(aP);
                     double cl, cu;  // couplings to the left / upper neighbour
                     if (k == 0 && l == 0) {
                         cl = ch_left0;
                     } else {
-                        cl = s_ch[o - 1];
+                        cl = lds<8 * KO(k) - 8>(aCH);
                     }
                     if (KO(k) + THREADS <= w || l < w) {  // first row: the previous block's couplings
                         const int j = base + l - w;
                         cu = j >= 0 ? __ldg(a.cv + j) : 0.0;
                     } else {
-                        cu = s_cv[o - w];
+                        cu = lds<8 * KO(k)>(aCV - wb);
                     }
                     acc = dg * pk;
-                    acc = __fma_rn(-s_ch[o], s_p[o + 1], acc);
-                    acc = __fma_rn(-cl, s_p[o - 1], acc);
-                    acc = __fma_rn(-s_cv[o], s_p[o + w], acc);
-                    acc = __fma_rn(-cu, s_p[o - w], acc);
+                    acc = __fma_rn(-lds<8 * KO(k)>(aCH), lds<8 * KO(k) + 8>(aP), acc);
+                    acc = __fma_rn(-cl, lds<8 * KO(k) - 8>(aP), acc);
+                    acc = __fma_rn(-lds<8 * KO(k)>(aCV), lds<8 * KO(k)>(aP + wb), acc);
+                    acc = __fma_rn(-cu, lds<8 * KO(k)>(aP - wb), acc);
                     const double ri = r[k];
-                    const double pq_ = s_pr[o] * acc;
+                    const double pq_ = lds<8 * KO(k)>(aPR) * acc;
                     v[0] = __fma_rn(pk, acc, v[0]);
                     v[5] = __fma_rn(pq_, ri, v[5]);
                     v[6] = __fma_rn(pq_, acc, v[6]);
@@ -361,7 +389,7 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
 #pragma unroll
                     for (int c = 0; c < 4; ++c) cur4[c] = nxt4[c];
                 }
-            }
+            });
             if (lane == 0) {
 #pragma unroll
                 for (int c = 1; c <= 4; ++c) v[c] = s_w1[warp * 4 + (c - 1)];
