@@ -34,7 +34,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define DCO_ABI_VERSION 1
+#define DCO_ABI_VERSION 2
 
 typedef enum dco_status {
     DCO_OK = 0,
@@ -227,6 +227,13 @@ typedef struct dco_frame_views {
     const float* composite;   /* full RGB */
     const uint8_t* mask;      /* full */
     const float* flow_past_u, *flow_past_v, *flow_future_u, *flow_future_v; /* quarter */
+    /* the frame's quarter-scale cost and aggregated volumes (stereo.cpp:106-218);
+     * volume_layout 0 = the reference's [y][x][d], 1 = slice-major [d][y][x]
+     * (the frame loop's fast path) */
+    const float* cost_volume;
+    const float* aggregated;
+    int volume_layout;
+    int num_disparities;
 } dco_frame_views;
 
 int dco_stream_create(dco_ctx* ctx, int full_w, int full_h, const dco_config* cfg,

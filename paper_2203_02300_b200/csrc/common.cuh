@@ -72,6 +72,7 @@ enum Slot : int {
     S_FLAG_BIN,
     S_FLAG_PEAK,
     S_FLAG_ASM,
+    S_FLAG_SLICE,
     S_HIST,
     S_STAGE,
     S_COUNT

@@ -1398,6 +1398,13 @@ void build_cross_windows(dco_ctx* ctx, const float* img, int w, int h, const dco
     launched(ctx, "k_arm_median");
 }
 
+void region_pack(dco_ctx* ctx, const uint8_t* l, const uint8_t* r, const uint8_t* u, const uint8_t* d, int w, int h,
+                 uint32_t* hinfo, uint32_t* vinfo) {
+    dim3 b(32, 8);
+    k_region_pack<<<grid2(w, h, b), b, 0, ctx->stream>>>(l, r, u, d, w, h, hinfo, vinfo);
+    launched(ctx, "k_region_pack");
+}
+
 void census_transform(dco_ctx* ctx, const float* img, int w, int h, int ww, int wh, uint64_t* out) {
     if (ww % 2 == 0 || wh % 2 == 0)
         fail(DCO_CONFIG, "census_transform: window dimensions must be odd");

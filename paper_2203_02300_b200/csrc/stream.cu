@@ -24,6 +24,14 @@ void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, in
 void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l, const uint8_t* r,
                      const uint8_t* u, const uint8_t* d, int max_arm, float* out);
 void select_disparity_wta(dco_ctx* ctx, const float* cost, int w, int h, int d_min, int nd, float* disp);
+// slice-major stereo core of the frame loop (stereo_slices.cu)
+bool stereo_slices_supported(int max_arm);
+void cost_volume_slices(dco_ctx* ctx, const float* left, const float* right, int w, int h, const uint8_t* l,
+                        const uint8_t* r, const uint8_t* u, const uint8_t* d, const dco_config* cfg, int max_arm,
+                        float* cost, int* unsafe);
+void aggregate_slices(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l, const uint8_t* r,
+                      const uint8_t* u, const uint8_t* d, int max_arm, const int* unsafe, float* agg);
+void wta_slices(dco_ctx* ctx, const float* agg, int w, int h, int d_min, int nd, float* disp);
 void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
                                 const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters, int bin_bound,
                                 int max_arm, float* out);
@@ -223,11 +231,22 @@ void run_frame(dco_stream* s, dco_frame_result* res) {
     // --- stereo on the middle pair (pipeline.cpp:184-195)
     build_cross_windows(ctx, s->left_q[mid], qw, qh, cfg, L, R, U, D);
     s->mark(DCO_SPAN_CROSS + 1);
-    compute_cost_volume(ctx, s->left_q[mid], s->right_q[mid], qw, qh, L, R, U, D, cfg, s->cost);
-    s->mark(DCO_SPAN_COST + 1);
-    aggregate_costs(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, s->agg);
-    s->mark(DCO_SPAN_AGGREGATE + 1);
-    select_disparity_wta(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
+    if (stereo_slices_supported(cfg->cross_arm_l1)) {
+        // slice-major cost volume + exact fixed-point aggregation (stereo_slices.cu)
+        int* unsafe = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, static_cast<size_t>(s->nd) * sizeof(int)));
+        cost_volume_slices(ctx, s->left_q[mid], s->right_q[mid], qw, qh, L, R, U, D, cfg, cfg->cross_arm_l1, s->cost,
+                           unsafe);
+        s->mark(DCO_SPAN_COST + 1);
+        aggregate_slices(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, unsafe, s->agg);
+        s->mark(DCO_SPAN_AGGREGATE + 1);
+        wta_slices(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
+    } else {
+        compute_cost_volume(ctx, s->left_q[mid], s->right_q[mid], qw, qh, L, R, U, D, cfg, s->cost);
+        s->mark(DCO_SPAN_COST + 1);
+        aggregate_costs(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, s->agg);
+        s->mark(DCO_SPAN_AGGREGATE + 1);
+        select_disparity_wta(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
+    }
     s->mark(DCO_SPAN_WTA + 1);
     refine_disparity_histogram(ctx, s->disp_wta, qw, qh, L, R, U, D, cfg->hist_iterations, cfg->d_max,
                                cfg->cross_arm_l1, s->disparity);
@@ -489,6 +508,10 @@ int dco_stream_views(const dco_stream* s, dco_frame_views* v) {
     v->flow_past_v = s->flow + nq;
     v->flow_future_u = s->flow + 2 * nq;
     v->flow_future_v = s->flow + 3 * nq;
+    v->cost_volume = s->cost;
+    v->aggregated = s->agg;
+    v->volume_layout = stereo_slices_supported(s->cfg.cross_arm_l1) ? 1 : 0;
+    v->num_disparities = s->nd;
     return DCO_OK;
 }
 
@@ -565,9 +588,16 @@ int dco_stereo_sparse_depth(dco_ctx* ctx, const float* left_q, const float* righ
         float* d1 = d0 + nq;
         uint8_t *L = arms, *R = arms + nq, *U = arms + 2 * nq, *D = arms + 3 * nq;
         build_cross_windows(ctx, left_q, w, h, cfg, L, R, U, D);
-        compute_cost_volume(ctx, left_q, right_q, w, h, L, R, U, D, cfg, cost);
-        aggregate_costs(ctx, cost, w, h, nd, L, R, U, D, cfg->cross_arm_l1, agg);
-        select_disparity_wta(ctx, agg, w, h, cfg->d_min, nd, d0);
+        if (stereo_slices_supported(cfg->cross_arm_l1)) {
+            int* unsafe = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, static_cast<size_t>(nd) * sizeof(int)));
+            cost_volume_slices(ctx, left_q, right_q, w, h, L, R, U, D, cfg, cfg->cross_arm_l1, cost, unsafe);
+            aggregate_slices(ctx, cost, w, h, nd, L, R, U, D, cfg->cross_arm_l1, unsafe, agg);
+            wta_slices(ctx, agg, w, h, cfg->d_min, nd, d0);
+        } else {
+            compute_cost_volume(ctx, left_q, right_q, w, h, L, R, U, D, cfg, cost);
+            aggregate_costs(ctx, cost, w, h, nd, L, R, U, D, cfg->cross_arm_l1, agg);
+            select_disparity_wta(ctx, agg, w, h, cfg->d_min, nd, d0);
+        }
         float* disp = disparity ? disparity : d1;
         refine_disparity_histogram(ctx, d0, w, h, L, R, U, D, cfg->hist_iterations, cfg->d_max, cfg->cross_arm_l1, disp);
         disparity_to_sparse_depth(ctx, disp, w, h, cfg, fw, fh, sparse);

@@ -74,6 +74,10 @@ class FrameViews(ctypes.Structure):
         ("flow_past_v", P),
         ("flow_future_u", P),
         ("flow_future_v", P),
+        ("cost_volume", P),
+        ("aggregated", P),
+        ("volume_layout", c_int),
+        ("num_disparities", c_int),
     ]
 
 
@@ -156,7 +160,7 @@ def load(path=LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.dco_abi_version() != 1:
+    if lib.dco_abi_version() != 2:
         raise RuntimeError("libdco_gpu.so ABI mismatch")
     _lib = lib
     return lib
