@@ -878,6 +878,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
 }  // namespace dco_gpu
 
 #include "pcg_tmem.cuh"
+#include "pcg_big.cuh"
 
 namespace dco_gpu {
 namespace {
@@ -902,6 +903,25 @@ OnchipKernel tmem_for(int ept) {
         case 6: return k_pcg_tmem<6>;
         case 7: return k_pcg_tmem<7>;
         case 8: return k_pcg_tmem<8>;
+        default: return nullptr;
+    }
+}
+typedef void (*BigKernel)(CGArgs, int, GridBar*, double*);
+BigKernel big_for(int ept) {
+    switch (ept) {
+        case 9: return k_pcg_big<9>;
+        case 10: return k_pcg_big<10>;
+        case 11: return k_pcg_big<11>;
+        case 12: return k_pcg_big<12>;
+        case 13: return k_pcg_big<13>;
+        case 14: return k_pcg_big<14>;
+        case 15: return k_pcg_big<15>;
+        case 16: return k_pcg_big<16>;
+        case 17: return k_pcg_big<17>;
+        case 18: return k_pcg_big<18>;
+        case 19: return k_pcg_big<19>;
+        case 20: return k_pcg_big<20>;
+        case 21: return k_pcg_big<21>;
         default: return nullptr;
     }
 }
@@ -1059,7 +1079,9 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     // the registers + shared-memory variant
     static const bool no_tmem = getenv("DCO_PCG_NO_TMEM") != nullptr;
     OnchipKernel kern = no_tmem ? onchip_for(threads, ept) : tmem_for(ept);
-    if (kern && smem <= kOnchipSmemMax && sms <= 1024) {
+    // DCO_PCG_FORCE_BIG=1 (tests): the large-frame kernel even when the state fits on chip
+    const bool force_big = getenv("DCO_PCG_FORCE_BIG") != nullptr;
+    if (kern && !force_big && smem <= kOnchipSmemMax && sms <= 1024) {
         // dynamic shared memory: exactly this launch's need (static scratch
         // comes on top, 227 KB per CTA in total)
         static int attr[2][17] = {};
@@ -1077,6 +1099,31 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
                                       params, smem);
         launched(ctx, no_tmem ? "k_pcg_onchip" : "k_pcg_tmem");
         return;
+    }
+    // larger frames: p on chip, q/rs in TMEM, r in registers, the rest L2-resident
+    {
+        const int ept_b = (chunk + kBigThreads - 1) / kBigThreads;
+        const size_t smem_b = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
+        BigKernel bk = big_for(ept_b < 9 ? 9 : ept_b);
+        if (bk && smem_b <= kOnchipSmemMax && sms <= 1024 && !getenv("DCO_PCG_NO_BIG")) {
+            static int attr_b[22] = {};
+            const int e = ept_b < 9 ? 9 : ept_b;
+            if (attr_b[e] < static_cast<int>(smem_b)) {
+                cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(bk),
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_b)),
+                           "smem attr");
+                attr_b[e] = static_cast<int>(smem_b);
+            }
+            int chunk_arg = chunk;
+            GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
+            cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
+            double* hb = static_cast<double*>(scratch(ctx, S_TMP1, 7 * n * sizeof(double)));
+            void* params[] = {&a, &chunk_arg, &bar, &hb};
+            launch_cooperative_serialized(ctx, reinterpret_cast<void*>(bk), dim3(sms), dim3(kBigThreads), params,
+                                          smem_b);
+            launched(ctx, "k_pcg_big");
+            return;
+        }
     }
     void* params[] = {&a};
     launch_cooperative_serialized(ctx, reinterpret_cast<void*>(k_pcg), dim3(nb), dim3(512), params, 0);
