@@ -907,21 +907,34 @@ OnchipKernel tmem_for(int ept) {
     }
 }
 typedef void (*BigKernel)(CGArgs, int, GridBar*, double*);
+BigKernel share_for(int ept) {
+    switch (ept) {
+        case 9: return k_pcg_big<9, kShareThreads, kShareCols, true>;
+        case 10: return k_pcg_big<10, kShareThreads, kShareCols, true>;
+        case 11: return k_pcg_big<11, kShareThreads, kShareCols, true>;
+        case 12: return k_pcg_big<12, kShareThreads, kShareCols, true>;
+        case 13: return k_pcg_big<13, kShareThreads, kShareCols, true>;
+        case 14: return k_pcg_big<14, kShareThreads, kShareCols, true>;
+        case 15: return k_pcg_big<15, kShareThreads, kShareCols, true>;
+        case 16: return k_pcg_big<16, kShareThreads, kShareCols, true>;
+        default: return nullptr;
+    }
+}
 BigKernel big_for(int ept) {
     switch (ept) {
-        case 9: return k_pcg_big<9>;
-        case 10: return k_pcg_big<10>;
-        case 11: return k_pcg_big<11>;
-        case 12: return k_pcg_big<12>;
-        case 13: return k_pcg_big<13>;
-        case 14: return k_pcg_big<14>;
-        case 15: return k_pcg_big<15>;
-        case 16: return k_pcg_big<16>;
-        case 17: return k_pcg_big<17>;
-        case 18: return k_pcg_big<18>;
-        case 19: return k_pcg_big<19>;
-        case 20: return k_pcg_big<20>;
-        case 21: return k_pcg_big<21>;
+        case 9: return k_pcg_big<9, kBigThreads, kBigCols, false>;
+        case 10: return k_pcg_big<10, kBigThreads, kBigCols, false>;
+        case 11: return k_pcg_big<11, kBigThreads, kBigCols, false>;
+        case 12: return k_pcg_big<12, kBigThreads, kBigCols, false>;
+        case 13: return k_pcg_big<13, kBigThreads, kBigCols, false>;
+        case 14: return k_pcg_big<14, kBigThreads, kBigCols, false>;
+        case 15: return k_pcg_big<15, kBigThreads, kBigCols, false>;
+        case 16: return k_pcg_big<16, kBigThreads, kBigCols, false>;
+        case 17: return k_pcg_big<17, kBigThreads, kBigCols, false>;
+        case 18: return k_pcg_big<18, kBigThreads, kBigCols, false>;
+        case 19: return k_pcg_big<19, kBigThreads, kBigCols, false>;
+        case 20: return k_pcg_big<20, kBigThreads, kBigCols, false>;
+        case 21: return k_pcg_big<21, kBigThreads, kBigCols, false>;
         default: return nullptr;
     }
 }
@@ -1081,6 +1094,30 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     OnchipKernel kern = no_tmem ? onchip_for(threads, ept) : tmem_for(ept);
     // DCO_PCG_FORCE_BIG=1 (tests): the large-frame kernel even when the state fits on chip
     const bool force_big = getenv("DCO_PCG_FORCE_BIG") != nullptr;
+    // DCO_PCG_SHARE=1: the co-residency variant (512 threads, p-only shared memory)
+    if (getenv("DCO_PCG_SHARE") && sms <= 1024) {
+        const int ept_s = std::max(9, (chunk + kShareThreads - 1) / kShareThreads);
+        const size_t smem_s = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
+        BigKernel sk = share_for(ept_s);
+        if (sk && smem_s <= kOnchipSmemMax) {
+            static int attr_s[17] = {};
+            if (attr_s[ept_s] < static_cast<int>(smem_s)) {
+                cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(sk),
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_s)),
+                           "smem attr");
+                attr_s[ept_s] = static_cast<int>(smem_s);
+            }
+            int chunk_arg = chunk;
+            GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
+            cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
+            double* hb = static_cast<double*>(scratch(ctx, S_TMP1, 7 * n * sizeof(double)));
+            void* params[] = {&a, &chunk_arg, &bar, &hb};
+            launch_cooperative_serialized(ctx, reinterpret_cast<void*>(sk), dim3(sms), dim3(kShareThreads), params,
+                                          smem_s);
+            launched(ctx, "k_pcg_share");
+            return;
+        }
+    }
     if (kern && !force_big && smem <= kOnchipSmemMax && sms <= 1024) {
         // dynamic shared memory: exactly this launch's need (static scratch
         // comes on top, 227 KB per CTA in total)

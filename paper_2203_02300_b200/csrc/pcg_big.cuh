@@ -18,11 +18,17 @@ namespace {
 
 constexpr int kBigThreads = 768;
 constexpr int kBigCols = 84;  // TMEM columns per warp (6 warps per lane quarter)
+// The co-residency variant (DCO_PCG_SHARE): 512 threads at <= 64 registers and
+// only p in shared memory, so the solve leaves half the register file and
+// ~150 KB of shared memory per SM to other streams' kernels; x and xs move to
+// TMEM too (4 warps per quarter: 128 columns = [q | rs | x | xs] x 16 slots).
+constexpr int kShareThreads = 512;
+constexpr int kShareCols = 128;
 
-template <int EPT>
-__global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk, GridBar* bar, double* hb) {
-    constexpr int THREADS = kBigThreads;
-    static_assert(4 * EPT <= kBigCols, "q | rs per slot in the warp's TMEM columns");
+template <int EPT, int THREADS, int COLS, bool XT>
+__global__ void __launch_bounds__(THREADS, XT ? 2 : 1) k_pcg_big(CGArgs a, int chunk, GridBar* bar, double* hb) {
+    constexpr int SL = XT ? 8 : 4;  // TMEM columns per slot
+    static_assert(SL * EPT <= COLS, "slot state in the warp's TMEM columns");
     extern __shared__ double sx[];  // p [w + chunk + w]
     __shared__ double sm[32 * 16];
     __shared__ double s_w1[32 * 4];
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // lane quarter = warp % 4; the 6 warps of a quarter own 84-column ranges
     const uint32_t tm = s_tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
-                        static_cast<uint32_t>((warp >> 2) * kBigCols);
+                        static_cast<uint32_t>((warp >> 2) * COLS);
     const double cterm = a.constant_term_dev ? *a.constant_term_dev : a.constant_term_host;
 
     // setup (densify.cpp:147-166)
@@ -80,7 +86,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
         r[k] = 0.0;
-        double ri = 0.0;
+        double ri = 0.0, xi0 = 0.0;
         if (DCO_OK(k)) {
             const int i = base + t + KO(k);
             const int xx = i % w, y = i / w;
@@ -101,8 +107,11 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
             r[k] = ri;
             s_p[KO(k)] = zi;
             a.prec[i] = pr;
-            a.x[i] = xi;
-            a.xs[i] = xi;
+            if (!XT) {
+                a.x[i] = xi;
+                a.xs[i] = xi;
+            }
+            xi0 = xi;
             hp0[i] = zi;
             tot[0] += b * b;
             tot[1] += ri * ri;
@@ -113,7 +122,12 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
         uint32_t v4[4];
         v4[0] = v4[1] = 0u;  // q
         d2u(ri, v4[2], v4[3]);
-        tm_st4(tm + 4 * k, v4);
+        tm_st4(tm + SL * k, v4);
+        if (XT) {  // x, xs
+            d2u(xi0, v4[0], v4[1]);
+            d2u(xi0, v4[2], v4[3]);
+            tm_st4(tm + SL * k + 4, v4);
+        }
     }
     barrier_reduce<5>(tot, bar, a.part, gen, sm, tot);
     const double bnorm = sqrt(tot[0]);
@@ -159,11 +173,13 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
             tm_wait_st();
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
-                uint32_t c4[4];
-                tm_ld4(tm + 4 * k, c4);  // q, rs
+                uint32_t c4[4], cx4[4];
+                tm_ld4(tm + SL * k, c4);  // q, rs
+                if (XT) tm_ld4(tm + SL * k + 4, cx4);  // x, xs
                 tm_wait_ld();
                 const double qk = u2d(c4[0], c4[1]);
                 double rsi = u2d(c4[2], c4[3]);
+                double xk_t = XT ? u2d(cx4[0], cx4[1]) : 0.0, xs_t = XT ? u2d(cx4[2], cx4[3]) : 0.0;
                 if (DCO_OK(k)) {
                     const int o = KO(k);
                     const int i = base + t + o;
@@ -171,16 +187,25 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
                     double ri = r[k];
                     const double pr = __ldcg(a.prec + i);
                     if (iter) {
-                        const double xk = __fma_rn(alpha, pk, __ldcg(a.x + i));
-                        __stcg(a.x + i, xk);
+                        const double xk = __fma_rn(alpha, pk, XT ? xk_t : __ldcg(a.x + i));
+                        if (XT) {
+                            xk_t = xk;
+                        } else {
+                            __stcg(a.x + i, xk);
+                        }
                         ri = __fma_rn(-alpha, qk, ri);
                         pk = __fma_rn(beta, pk, pr * ri);
                         r[k] = ri;
                         s_p[o] = pk;
                         if (eta > 0.0) {
                             rsi = __fma_rn(eta, ri - rsi, rsi);
-                            const double xsi = __ldcg(a.xs + i);
-                            __stcg(a.xs + i, __fma_rn(eta, xk - xsi, xsi));
+                            const double xsi = XT ? xs_t : __ldcg(a.xs + i);
+                            const double xsn = __fma_rn(eta, xk - xsi, xsi);
+                            if (XT) {
+                                xs_t = xsn;
+                            } else {
+                                __stcg(a.xs + i, xsn);
+                            }
                         }
                     }
                     const double e = ri - rsi;
@@ -196,7 +221,13 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
                 if (iter && eta > 0.0) {  // warp-uniform
                     uint32_t s2[2];
                     d2u(rsi, s2[0], s2[1]);
-                    tm_st2(tm + 4 * k + 2, s2);
+                    tm_st2(tm + SL * k + 2, s2);
+                }
+                if (XT && iter) {  // x (and xs, unchanged when eta == 0)
+                    uint32_t s4[4];
+                    d2u(xk_t, s4[0], s4[1]);
+                    d2u(xs_t, s4[2], s4[3]);
+                    tm_st4(tm + SL * k + 4, s4);
                 }
             }
 #pragma unroll
@@ -214,7 +245,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
                 uint32_t c2[2];
-                tm_ld2(tm + 4 * k + 2, c2);  // rs
+                tm_ld2(tm + SL * k + 2, c2);  // rs
                 tm_wait_ld();
                 const double rsi = u2d(c2[0], c2[1]);
                 double acc = 0.0;
@@ -240,7 +271,7 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
                 }
                 uint32_t s2[2];
                 d2u(acc, s2[0], s2[1]);
-                tm_st2(tm + 4 * k, s2);
+                tm_st2(tm + SL * k, s2);
             }
             if (lane == 0) {
 #pragma unroll
@@ -269,9 +300,18 @@ __global__ void __launch_bounds__(kBigThreads, 1) k_pcg_big(CGArgs a, int chunk,
             ++iter;
         }
     }
-    // dense map from xs (already in a.xs for the objective's stencil)
-    for (int i = base + t; i < base + size; i += THREADS) a.dense[i] = static_cast<float>(dmax0(__ldcg(a.xs + i)));
+    // dense map from xs (in a.xs for the objective's stencil)
     tm_wait_st();
+    if (XT) {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            uint32_t v2[2];
+            tm_ld2(tm + SL * k + 6, v2);
+            tm_wait_ld();
+            if (DCO_OK(k)) a.xs[base + t + KO(k)] = u2d(v2[0], v2[1]);
+        }
+    }
+    for (int i = base + t; i < base + size; i += THREADS) a.dense[i] = static_cast<float>(dmax0(__ldcg(a.xs + i)));
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     {
         double z[1] = {0.0}, dummy[1];
