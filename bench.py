@@ -269,24 +269,18 @@ def run_ours(args, world, rank, local):
     import torch
 
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if dist:
-            dist.barrier()
-
     from paper_2203_02300_b200 import dco
     from paper_2203_02300_b200.config import Config
+    from paper_2203_02300_b200.sharding import Group, stream_seeds
     from paper_2203_02300_b200.synth import StereoVideo
+
+    group = Group(world, local, "nccl")
+    barrier = group.barrier
 
     S = args.streams
     cfg = Config(d_max=D - 1)
     nframes = 32
-    vids = [StereoVideo(W, H, seed=61 + 97 * rank + s) for s in range(S)]
+    vids = [StereoVideo(W, H, seed=sd) for sd in stream_seeds(rank, S)]
     host = [[v.frame(i) for i in range(nframes)] for v in vids]
     dev_l = [torch.from_numpy(np.stack([f[0] for f in h])).cuda() for h in host]
     dev_r = [torch.from_numpy(np.stack([f[1] for f in h])).cuda() for h in host]
@@ -375,15 +369,11 @@ def run_ours(args, world, rank, local):
     e2e_total = 1000.0 * (time.perf_counter() - w0)
     barrier()
 
-    tot = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    total_ms, e2e_total = tot.tolist()
+    total_ms, e2e_total = group.max_over_ranks([total_ms, e2e_total], device="cuda")
     if rank != 0:
         for st in streams:
             st.close()
-        if dist:
-            dist.destroy_process_group()
+        group.close()
         return
 
     frames = world * S * args.steps
@@ -440,8 +430,7 @@ def run_ours(args, world, rank, local):
     for st in streams:
         st.close()
     print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    group.close()
 
 
 def cpu_baseline(s, dev_l, dev_r, lefts, rights, cfg, i, nframes):

@@ -64,6 +64,11 @@ def _compile(src):
         if r.stderr.strip():
             sys.stderr.write(r.stderr)
         os.replace(obj + ".tmp", obj)
+        # drop this source's stale objects (older digests)
+        stem = src[:-3] + "."
+        for f in os.listdir(OBJ):
+            if f.startswith(stem) and f.endswith(".o") and os.path.join(OBJ, f) != obj:
+                os.remove(os.path.join(OBJ, f))
     return obj
 
 
