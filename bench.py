@@ -14,7 +14,7 @@ pipeline streams concurrently (own dco_ctx + CUDA stream each; frames shard
 across streams and GPUs, no data-path collective: "scaling": "weak"). A step
 is one frame on every stream. The timed region is bracketed by a barrier +
 cuda.synchronize; the reported time is the max over ranks. L2 is flushed
-(256 MiB memset) before every frame inside the timed region (conservative).
+(160 MiB memset; the L2 is 126 MB) before every frame inside the timed region (conservative).
 
 `value` times frames whose u8 inputs are already in HBM. `e2e` times the same
 steps through the host-buffer C-ABI (dco_stream_push_gray8_host): pinned u8
@@ -298,7 +298,7 @@ def run_ours(args, world, rank, local):
             st = dco.Stream(W, H, cfg, ctx=dco.new_context(tstreams[s]))
             st.set_virtual(vrgb, vdepth)
             streams.append(st)
-    flush = [torch.empty(256 << 20, dtype=torch.uint8, device="cuda") for _ in range(S)]
+    flush = [torch.empty(160 << 20, dtype=torch.uint8, device="cuda") for _ in range(S)]  # > the 126 MB L2
     pos = [0] * S
 
     def push(s, want=False):
@@ -407,7 +407,7 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
         "config": {"workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+composite)",
                    "width": W, "height": H, "disparities": D, "streams_per_gpu": S, "frames_per_step": S * world,
-                   "l2": "flushed (256 MiB memset) before every frame, inside the timed region",
+                   "l2": "flushed (160 MiB memset, L2 is 126 MB) before every frame, inside the timed region",
                    "parallelism": "stream-sharded x%d, %d concurrent streams per GPU" % (world, S)},
         "roofline": roof,
         "aggregation_roofline": {"achieved": agg_ab / (per_frame["aggregate"] / 1000.0) / 1e9, "peak": peak,

@@ -158,6 +158,37 @@ __global__ void k_census(const float* __restrict__ img, int w, int h, int rw, in
     out[static_cast<size_t>(y) * w + x] = bits;
 }
 
+// census_transform over a shared-memory tile (the clamped window of a 32x8
+// block staged once), both images of a stereo pair in one launch (z).
+__global__ void __launch_bounds__(256) k_census_tiled(const float* __restrict__ img0, const float* __restrict__ img1,
+                                                      int w, int h, int rw, int rh, uint64_t* __restrict__ out0,
+                                                      uint64_t* __restrict__ out1) {
+    extern __shared__ float tile[];  // (32 + 2 rw) x (8 + 2 rh)
+    const float* img = blockIdx.z ? img1 : img0;
+    uint64_t* out = blockIdx.z ? out1 : out0;
+    const int tw = 32 + 2 * rw, th = 8 + 2 * rh;
+    const int x0 = blockIdx.x * 32 - rw, y0 = blockIdx.y * 8 - rh;
+    for (int i = threadIdx.y * 32 + threadIdx.x; i < tw * th; i += 256) {
+        const int ty = i / tw, tx = i - ty * tw;
+        const int yy = min(max(y0 + ty, 0), h - 1), xx = min(max(x0 + tx, 0), w - 1);
+        tile[i] = img[static_cast<size_t>(yy) * w + xx];
+    }
+    __syncthreads();
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    if (x >= w || y >= h) return;
+    const float* c = tile + (threadIdx.y + rh) * tw + threadIdx.x + rw;
+    const float center = *c;
+    uint64_t bits = 0;
+    for (int dy = -rh; dy <= rh; ++dy) {
+        const float* row = c + dy * tw;
+        for (int dx = -rw; dx <= rw; ++dx) {
+            if (dx == 0 && dy == 0) continue;
+            bits = (bits << 1) | (row[dx] < center ? 1ull : 0ull);
+        }
+    }
+    out[static_cast<size_t>(y) * w + x] = bits;
+}
+
 // ------------------------------------------------------------ cost volume --
 // compute_cost_volume, stereo.cpp:106-150. One thread per (pixel, d): the
 // warp spans consecutive d of one pixel, so the [p][d] store is coalesced and
@@ -1405,6 +1436,16 @@ void region_pack(dco_ctx* ctx, const uint8_t* l, const uint8_t* r, const uint8_t
     launched(ctx, "k_region_pack");
 }
 
+// census of a stereo pair in one tiled launch (the cost volume's inputs)
+void census_pair(dco_ctx* ctx, const float* left, const float* right, int w, int h, int ww, int wh,
+                 uint64_t* out_l, uint64_t* out_r) {
+    const int rw = ww / 2, rh = wh / 2;
+    const size_t smem = static_cast<size_t>(32 + 2 * rw) * (8 + 2 * rh) * sizeof(float);
+    k_census_tiled<<<dim3((w + 31) / 32, (h + 7) / 8, 2), dim3(32, 8), smem, ctx->stream>>>(left, right, w, h, rw,
+                                                                                           rh, out_l, out_r);
+    launched(ctx, "k_census_tiled");
+}
+
 void census_transform(dco_ctx* ctx, const float* img, int w, int h, int ww, int wh, uint64_t* out) {
     if (ww % 2 == 0 || wh % 2 == 0)
         fail(DCO_CONFIG, "census_transform: window dimensions must be odd");
@@ -1420,8 +1461,7 @@ void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, in
     validate_config(cfg);
     const size_t n = static_cast<size_t>(w) * h;
     uint64_t* census = static_cast<uint64_t*>(scratch(ctx, S_CENSUS, n * 16));
-    census_transform(ctx, left, w, h, cfg->census_window_w, cfg->census_window_h, census);
-    census_transform(ctx, right, w, h, cfg->census_window_w, cfg->census_window_h, census + n);
+    census_pair(ctx, left, right, w, h, cfg->census_window_w, cfg->census_window_h, census, census + n);
     CostParams hp;
     hp.w = w;
     hp.h = h;
