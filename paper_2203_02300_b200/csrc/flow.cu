@@ -60,6 +60,22 @@ __device__ __forceinline__ float sample_bilinear(const float* img, int w, int h,
     return top * (1.0f - fy) + bot * fy;
 }
 
+// downsample_half (pyramid.cpp:5-17) of up to three same-size images in one
+// launch (z = image): one pyramid level of the from / to / to frames.
+struct PyrLevel {
+    const float* src[3];
+    float* dst[3];
+};
+__global__ void k_pyr_level(const __grid_constant__ PyrLevel pl, int w, int ow, int oh) {
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= ow || y >= oh) return;
+    const float* r0 = pl.src[blockIdx.z] + static_cast<size_t>(2 * y) * w + 2 * x;
+    const float* r1 = r0 + w;
+    float sum = r0[0] + r0[1] + r1[0] + r1[1];
+    pl.dst[blockIdx.z][static_cast<size_t>(y) * ow + x] = sum * 0.25f;
+}
+
 // upsample_flow, flow.cpp:39-62. z = direction.
 __global__ void k_flow_upsample(const float* __restrict__ cu, const float* __restrict__ cv, int cw,
                                 int ch, float* __restrict__ fu, float* __restrict__ fv, int fw,
@@ -322,16 +338,25 @@ void compute_flow_multi(dco_ctx* ctx, const float* from, const float* const* to,
     for (int k = 0; k < dirs; ++k) p_to[k][0] = to[k];
     for (int l = 1; l < levels; ++l) {
         size_t n = static_cast<size_t>(lv[l].w) * lv[l].h;
+        PyrLevel pl{};
         float* f = pyr + off;
         off += n;
-        downsample_half(ctx, p_from[l - 1], lv[l - 1].w, lv[l - 1].h, f);
+        pl.src[0] = p_from[l - 1];
+        pl.dst[0] = f;
         p_from[l] = f;
         for (int k = 0; k < dirs; ++k) {
             float* t = pyr + off;
             off += n;
-            downsample_half(ctx, p_to[k][l - 1], lv[l - 1].w, lv[l - 1].h, t);
+            pl.src[1 + k] = p_to[k][l - 1];
+            pl.dst[1 + k] = t;
             p_to[k][l] = t;
         }
+        // every level of the three pyramids in one launch (pyramid.cpp:5-17)
+        require(lv[l - 1].w >= 2 && lv[l - 1].h >= 2, "downsample_half: dimensions must be at least 2x2");
+        dim3 bd(32, 8);
+        k_pyr_level<<<dim3((lv[l].w + 31) / 32, (lv[l].h + 7) / 8, 1 + dirs), bd, 0, ctx->stream>>>(
+            pl, lv[l - 1].w, lv[l].w, lv[l].h);
+        launched(ctx, "k_pyr_level");
     }
     float* res = static_cast<float*>(scratch(ctx, S_FLOW_PATCH, max_patches * 3 * 2 * sizeof(float)));
     // field ping-pong: [buf][dir][u|v][max_level]
