@@ -1090,7 +1090,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     const size_t smem = (static_cast<size_t>(chunk) * 4 + 2 * static_cast<size_t>(w)) * sizeof(double);
     // registers + TMEM + shared memory (pcg_tmem.cuh); DCO_PCG_NO_TMEM=1 selects
     // the registers + shared-memory variant
-    static const bool no_tmem = getenv("DCO_PCG_NO_TMEM") != nullptr;
+    const bool no_tmem = getenv("DCO_PCG_NO_TMEM") != nullptr;
     OnchipKernel kern = no_tmem ? onchip_for(threads, ept) : tmem_for(ept);
     // DCO_PCG_FORCE_BIG=1 (tests): the large-frame kernel even when the state fits on chip
     const bool force_big = getenv("DCO_PCG_FORCE_BIG") != nullptr;

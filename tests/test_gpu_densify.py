@@ -71,15 +71,17 @@ def _solve_both(gpu, ref, sparse, edges, m_fuse, m_i, pre, cfg):
     return N(got), gst, want, st
 
 
-@pytest.mark.parametrize("variant", ["tmem", "big", "share"])
+VARIANT_ENV = {"tmem": None, "onchip": "DCO_PCG_NO_TMEM", "big": "DCO_PCG_FORCE_BIG", "share": "DCO_PCG_SHARE"}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANT_ENV))
 @pytest.mark.parametrize("seed,with_pre", [(5150, False), (5151, True), (77, False)])
 def test_solve_small_within_tolerance(gpu, ref, seed, with_pre, variant, monkeypatch):
-    """big: the large-frame kernel (x/xs/coefficients in L2) forced on a small
-    system (DCO_PCG_FORCE_BIG); share: the co-residency kernel (DCO_PCG_SHARE)."""
-    if variant == "big":
-        monkeypatch.setenv("DCO_PCG_FORCE_BIG", "1")
-    if variant == "share":
-        monkeypatch.setenv("DCO_PCG_SHARE", "1")
+    """Every solver variant: tmem (default), onchip (registers + shared memory,
+    DCO_PCG_NO_TMEM), big (x/xs/coefficients in L2, forced on a small system)
+    and share (the co-residency kernel)."""
+    if VARIANT_ENV[variant]:
+        monkeypatch.setenv(VARIANT_ENV[variant], "1")
     cfg = Config(solver_tol=1e-12, solver_max_iter=3000)
     got, gst, want, st = _solve_both(gpu, ref, *random_inputs(16, 16, seed, with_pre), cfg)
     d = np.abs(got.astype(np.float64) - want)
@@ -88,14 +90,12 @@ def test_solve_small_within_tolerance(gpu, ref, seed, with_pre, variant, monkeyp
     assert gst.objective_final <= gst.objective_initial + 1e-9
 
 
-@pytest.mark.parametrize("variant", ["tmem", "big", "share"])
+@pytest.mark.parametrize("variant", sorted(VARIANT_ENV))
 def test_solve_scene_within_tolerance(gpu, ref, variant, monkeypatch):
     """A real frame's system (640x360 full res) with and without d_pre, on each
     solver variant."""
-    if variant == "big":
-        monkeypatch.setenv("DCO_PCG_FORCE_BIG", "1")
-    if variant == "share":
-        monkeypatch.setenv("DCO_PCG_SHARE", "1")
+    if VARIANT_ENV[variant]:
+        monkeypatch.setenv(VARIANT_ENV[variant], "1")
     cfg = Config(d_max=63)
     fs = [scene(ref, 640, 360, index=i, seed=61) for i in range(4)]
     q = [ref.downsample_half(f["left"]) for f in fs]
