@@ -201,6 +201,19 @@ int dco_solve_dense_depth(dco_ctx* ctx, const dco_system* sys, const dco_config*
 int dco_composite(dco_ctx* ctx, const float* real_rgb, const float* dense, const float* virt_rgb,
                   const float* virt_depth, int w, int h, float* out_rgb, uint8_t* mask);
 
+/* ---- virtual layer (occlude.hpp:36-48) ----------------- */
+/* transform_mesh, occlude.cpp:78-87. vertices/out: 3*num_vertices floats
+ * (device); pose: 16 doubles, row-major (HOST). */
+int dco_transform_mesh(dco_ctx* ctx, const float* vertices, int num_vertices, const double* pose,
+                       float* out);
+/* render_virtual, occlude.cpp:107-169. vertices / colors: 3 floats per vertex,
+ * triangles: 3 ints per triangle (device). rgb: 3*w*h floats (0 where nothing
+ * covers), depth: w*h floats (NaN where nothing covers). Bit-exact with the
+ * reference's index-ordered z-buffer (tile-binned, per-pixel ordered). */
+int dco_render_virtual(dco_ctx* ctx, const float* vertices, const int* triangles, const float* colors,
+                       int num_triangles, double focal_px, double cx, double cy, int width, int height,
+                       float* rgb, float* depth);
+
 /* ---- frame orchestration (pipeline.cpp:136-258) ------------------------- */
 /* One stream of the pipeline: the KeyframeBuffer window (flow.cpp:10-18), the
  * previous dense map chain (pipeline.cpp:133, 235) and the Unsolvable fallback
@@ -243,6 +256,17 @@ void dco_stream_destroy(dco_stream* s);
  * copied into the stream). NULL clears it: the frame then passes the real
  * colour through with an empty mask (pipeline.cpp:254-257). */
 int dco_stream_set_virtual(dco_stream* s, const float* virt_rgb, const float* virt_depth);
+/* Virtual mesh rendered on the device for every composited frame
+ * (pipeline.cpp:247-252: transform_mesh by the frame's pose, then
+ * render_virtual with focal_px and the image centre). HOST arrays, copied:
+ * vertices / colors 3 floats per vertex, triangles 3 ints each. Takes
+ * precedence over dco_stream_set_virtual; NULL vertices clear it. */
+int dco_stream_set_mesh(dco_stream* s, const float* vertices, int num_vertices, const int* triangles,
+                        int num_triangles, const float* colors);
+/* Pose (16 doubles, row-major, host) of the NEXT pushed frame -- the manifest
+ * record's pose (pipeline.cpp:42-47). NULL: that frame's mesh is not
+ * transformed. */
+int dco_stream_set_next_pose(dco_stream* s, const double* pose);
 /* Push one frame (device buffers): 8-bit left/right gray and the left colour
  * as 8-bit RGB (read_color / read_gray of the same PGM give rgb = gray x3;
  * rgb8 may be NULL to mean exactly that). */

@@ -57,6 +57,8 @@ def lib():
                                           ctypes.POINTER(D), ctypes.POINTER(D), P, I]),
             "ref_composite": (I, [P, P, P, P, I, I, P, P]),
             "ref_render_cube": (I, [ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, D, I, I, P, P]),
+            "ref_render_virtual": (I, [P, I, P, I, P, P, D, D, D, I, I, P, P]),
+            "ref_transform_mesh": (I, [P, I, P, P]),
             "ref_pipeline_frame": (I, [I, I, P, P, P, P, P, P, P, P, P, CFG, P, P, P, P, P, ctypes.POINTER(I),
                                        ctypes.POINTER(D)]),
         }
@@ -328,6 +330,25 @@ def render_cube(w, h, focal_px, cx=0.0, cy=0.0, cz=1.5, side=0.3):
     vdepth = np.empty((h, w), np.float32)
     _check(lib().ref_render_cube(cx, cy, cz, side, focal_px, w, h, _p(vrgb), _p(vdepth)))
     return vrgb, vdepth
+
+
+def render_virtual(verts, tris, colors, focal_px, cx, cy, w, h, pose=None):
+    """transform_mesh (when pose is given) + render_virtual, occlude.cpp:78-169."""
+    verts, tris, colors = _c(verts, np.float32), _c(tris, np.int32), _c(colors, np.float32)
+    pose_p = _p(_c(pose, np.float64)) if pose is not None else None
+    vrgb = np.empty((h, w, 3), np.float32)
+    vdepth = np.empty((h, w), np.float32)
+    _check(lib().ref_render_virtual(_p(verts), len(verts), _p(tris), len(tris), _p(colors), pose_p, focal_px, cx, cy,
+                                    w, h, _p(vrgb), _p(vdepth)))
+    return vrgb, vdepth
+
+
+def transform_mesh(verts, pose):
+    """transform_mesh, occlude.cpp:78-87."""
+    verts = _c(verts, np.float32)
+    out = np.empty_like(verts)
+    _check(lib().ref_transform_mesh(_p(verts), len(verts), _p(_c(pose, np.float64)), _p(out)))
+    return out
 
 
 def pipeline_frame(past_q, mid_q, future_q, mid_gray, right_q, mid_rgb, d_pre, vrgb, vdepth, cfg):

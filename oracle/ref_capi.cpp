@@ -513,6 +513,45 @@ int ref_render_cube(float cx, float cy, float cz, float side, double focal_px, i
     });
 }
 
+// transform_mesh + render_virtual (occlude.cpp:78-169) on an arbitrary mesh:
+// vertices / colours are nv x 3 floats, triangles nt x 3 ints; pose (16
+// doubles, row-major) may be NULL (no transform, pipeline.cpp:249-250).
+int ref_render_virtual(const float* verts, int nv, const int* tris, int nt, const float* colors,
+                       const double* pose, double focal_px, double cx, double cy, int w, int h, float* vrgb,
+                       float* vdepth) {
+    return guarded([&] {
+        TriangleMesh m;
+        for (int i = 0; i < nv; ++i) {
+            m.vertices.push_back({verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]});
+            m.colors.push_back({colors[3 * i], colors[3 * i + 1], colors[3 * i + 2]});
+        }
+        for (int t = 0; t < nt; ++t) m.triangles.push_back({tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]});
+        if (pose) {
+            std::array<double, 16> p;
+            for (int i = 0; i < 16; ++i) p[i] = pose[i];
+            m = transform_mesh(m, p);
+        }
+        VirtualLayer v = render_virtual(m, focal_px, cx, cy, w, h);
+        copy_out(v.color.data, vrgb);
+        copy_out(v.depth.data, vdepth);
+    });
+}
+
+int ref_transform_mesh(const float* verts, int nv, const double* pose, float* out) {
+    return guarded([&] {
+        TriangleMesh m;
+        for (int i = 0; i < nv; ++i) {
+            m.vertices.push_back({verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]});
+            m.colors.push_back({0.0f, 0.0f, 0.0f});
+        }
+        std::array<double, 16> p;
+        for (int i = 0; i < 16; ++i) p[i] = pose[i];
+        TriangleMesh o = transform_mesh(m, p);
+        for (int i = 0; i < nv; ++i)
+            for (int k = 0; k < 3; ++k) out[3 * i + k] = o.vertices[i][k];
+    });
+}
+
 // One composited frame of run_pipeline (pipeline.cpp:183-258) on in-memory
 // inputs: past/middle/future quarter lefts, the middle's full gray, quarter
 // right, colour, optional previous dense map and virtual layer. Outputs: dense

@@ -73,6 +73,8 @@ enum Slot : int {
     S_FLAG_PEAK,
     S_FLAG_ASM,
     S_FLAG_SLICE,
+    S_RENDER,
+    S_RENDER_LIST,
     S_HIST,
     S_STAGE,
     S_COUNT

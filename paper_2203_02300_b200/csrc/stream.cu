@@ -24,6 +24,10 @@ void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, in
 void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l, const uint8_t* r,
                      const uint8_t* u, const uint8_t* d, int max_arm, float* out);
 void select_disparity_wta(dco_ctx* ctx, const float* cost, int w, int h, int d_min, int nd, float* disp);
+// render.cu
+void transform_mesh(dco_ctx* ctx, const float* verts, int nv, const double* pose, float* out);
+void render_virtual(dco_ctx* ctx, const float* verts, const int* tris, const float* colors, int nt, double focal_px,
+                    double cx, double cy, int w, int h, float* rgb, float* depth);
 // slice-major stereo core of the frame loop (stereo_slices.cu)
 bool stereo_slices_supported(int max_arm);
 void cost_volume_slices(dco_ctx* ctx, const float* left, const float* right, int w, int h, const uint8_t* l,
@@ -172,6 +176,17 @@ struct dco_stream {
     float* vrgb = nullptr;
     float* vdepth = nullptr;
     bool has_virtual = false;
+    // virtual mesh rendered per frame (occlude.cpp:107-169, pipeline.cpp:247-252)
+    float* mesh_v = nullptr;  // device copies
+    int* mesh_t = nullptr;
+    float* mesh_c = nullptr;
+    float* mesh_posed = nullptr;
+    int mesh_nv = 0, mesh_nt = 0;
+    bool has_mesh = false;
+    double pose[3][16] = {};  // per window slot: the frame's manifest pose
+    bool pose_set[3] = {};
+    double next_pose[16] = {};
+    bool next_pose_set = false;
     void* host_out = nullptr;
     // optional per-span CUDA-event timing (StageTimings, pipeline.hpp:27-46)
     // A ring of kRing event sets so the host never waits on the frame it just
@@ -196,6 +211,11 @@ struct dco_stream {
         }
         ++timed_frames;
         pending[set] = false;
+    }
+    void take_pose(int slot) {  // the pose set for this push (pipeline.cpp:249: the record's pose)
+        pose_set[slot] = next_pose_set;
+        for (int i = 0; i < 16; ++i) pose[slot][i] = next_pose[i];
+        next_pose_set = false;
     }
     void begin_frame() {  // before the frame's first kernel
         if (!timing) return;
@@ -283,8 +303,19 @@ void run_frame(dco_stream* s, dco_frame_result* res) {
     launched(ctx, "k_keep_dense");
     s->mark(DCO_SPAN_SOLVE + 1);
     // --- composite (pipeline.cpp:247-258)
-    composite(ctx, s->rgb[mid], s->dense, s->has_virtual ? s->vrgb : nullptr,
-              s->has_virtual ? s->vdepth : nullptr, fw, fh, s->comp, s->mask);
+    if (s->has_mesh) {
+        // render_virtual of the (posed) mesh for the middle frame (pipeline.cpp:249-252)
+        const float* verts = s->mesh_v;
+        if (s->pose_set[mid]) {
+            transform_mesh(ctx, s->mesh_v, s->mesh_nv, s->pose[mid], s->mesh_posed);
+            verts = s->mesh_posed;
+        }
+        render_virtual(ctx, verts, s->mesh_t, s->mesh_c, s->mesh_nt, cfg->focal_px, fw / 2.0, fh / 2.0, fw, fh,
+                       s->vrgb, s->vdepth);
+    }
+    const bool layer = s->has_mesh || s->has_virtual;
+    composite(ctx, s->rgb[mid], s->dense, layer ? s->vrgb : nullptr, layer ? s->vdepth : nullptr, fw, fh, s->comp,
+              s->mask);
     s->mark(DCO_SPAN_COMPOSITE + 1);
     if (s->timing) s->pending[s->cur_set] = true;
     if (res) {
@@ -406,6 +437,51 @@ int dco_stream_set_virtual(dco_stream* s, const float* vrgb, const float* vdepth
     });
 }
 
+int dco_stream_set_mesh(dco_stream* s, const float* vertices, int num_vertices, const int* triangles,
+                        int num_triangles, const float* colors) {
+    if (!s) return DCO_INPUT;
+    return guarded(s->ctx, [&] {
+        if (!vertices || !triangles || !colors || num_vertices <= 0) {
+            s->has_mesh = false;
+            return;
+        }
+        require(num_triangles >= 0, "set_mesh: negative triangle count");
+        for (int t = 0; t < 3 * num_triangles; ++t)
+            require(triangles[t] >= 0 && triangles[t] < num_vertices, "set_mesh: triangle index out of range");
+        const size_t nf = static_cast<size_t>(s->fw) * s->fh;
+        if (!s->vrgb) {
+            s->vrgb = s->alloc<float>(3 * nf);
+            s->vdepth = s->alloc<float>(nf);
+        }
+        if (num_vertices > s->mesh_nv || !s->mesh_v) {
+            s->mesh_v = s->alloc<float>(3 * static_cast<size_t>(num_vertices));
+            s->mesh_c = s->alloc<float>(3 * static_cast<size_t>(num_vertices));
+            s->mesh_posed = s->alloc<float>(3 * static_cast<size_t>(num_vertices));
+        }
+        if (num_triangles > s->mesh_nt || !s->mesh_t)
+            s->mesh_t = s->alloc<int>(3 * static_cast<size_t>(std::max(num_triangles, 1)));
+        cuda_check(cudaMemcpy(s->mesh_v, vertices, 12 * static_cast<size_t>(num_vertices), cudaMemcpyHostToDevice),
+                   "h2d");
+        cuda_check(cudaMemcpy(s->mesh_c, colors, 12 * static_cast<size_t>(num_vertices), cudaMemcpyHostToDevice),
+                   "h2d");
+        if (num_triangles)
+            cuda_check(cudaMemcpy(s->mesh_t, triangles, 12 * static_cast<size_t>(num_triangles),
+                                  cudaMemcpyHostToDevice),
+                       "h2d");
+        s->mesh_nv = num_vertices;
+        s->mesh_nt = num_triangles;
+        s->has_mesh = true;
+    });
+}
+
+int dco_stream_set_next_pose(dco_stream* s, const double* pose) {
+    if (!s) return DCO_INPUT;
+    s->next_pose_set = pose != nullptr;
+    if (pose)
+        for (int i = 0; i < 16; ++i) s->next_pose[i] = pose[i];
+    return DCO_OK;
+}
+
 int dco_stream_push_gray8(dco_stream* s, const uint8_t* left8, const uint8_t* right8, const uint8_t* rgb8,
                           dco_frame_result* res) {
     if (!s) return DCO_INPUT;
@@ -413,6 +489,7 @@ int dco_stream_push_gray8(dco_stream* s, const uint8_t* left8, const uint8_t* ri
         dco_ctx* ctx = s->ctx;
         if (s->pushed + 1 >= 3) s->begin_frame();
         int slot = static_cast<int>(s->pushed % 3);
+        s->take_pose(slot);
         ingest_gray8(ctx, left8, s->fw, s->fh, s->gray[slot], s->left_q[slot]);
         ingest_gray8(ctx, right8, s->fw, s->fh, nullptr, s->right_q[slot]);
         size_t nf = static_cast<size_t>(s->fw) * s->fh;
@@ -429,6 +506,7 @@ int dco_stream_push_f32(dco_stream* s, const float* left, const float* right, co
         dco_ctx* ctx = s->ctx;
         if (s->pushed + 1 >= 3) s->begin_frame();
         int slot = static_cast<int>(s->pushed % 3);
+        s->take_pose(slot);
         size_t nf = static_cast<size_t>(s->fw) * s->fh;
         cuda_check(cudaMemcpyAsync(s->gray[slot], left, nf * 4, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
         downsample_half(ctx, left, s->fw, s->fh, s->left_q[slot]);
@@ -450,6 +528,7 @@ int dco_stream_push_gray8_host(dco_stream* s, const uint8_t* left8, const uint8_
         cuda_check(cudaMemcpyAsync(staging + nf, right8, nf, cudaMemcpyHostToDevice, ctx->stream), "h2d");
         if (s->pushed + 1 >= 3) s->begin_frame();
         int slot = static_cast<int>(s->pushed % 3);
+        s->take_pose(slot);
         ingest_gray8(ctx, staging, s->fw, s->fh, s->gray[slot], s->left_q[slot]);
         ingest_gray8(ctx, staging + nf, s->fw, s->fh, nullptr, s->right_q[slot]);
         k_rgb_from_u8<<<blocks_for(nf, 256), 256, 0, ctx->stream>>>(staging, nullptr, nf, s->rgb[slot]);

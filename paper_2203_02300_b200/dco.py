@@ -415,6 +415,26 @@ def composite(real_rgb, dense, virt_rgb, virt_depth):
     return out, mask
 
 
+# --------------------------------------------------------- virtual layer ---
+def transform_mesh(vertices, pose):
+    """transform_mesh, occlude.cpp:78-87: vertices (n, 3) float CUDA tensor,
+    pose 16 row-major doubles (host sequence)."""
+    n = vertices.shape[0]
+    out = torch.empty_like(vertices)
+    pose_h = (ctypes.c_double * 16)(*[float(v) for v in pose])
+    _call(_lib().dco_transform_mesh, _p(vertices), n, ctypes.cast(pose_h, ctypes.c_void_p), _p(out))
+    return out
+
+
+def render_virtual(vertices, triangles, colors, focal_px, cx, cy, width, height):
+    """render_virtual, occlude.cpp:107-169: (rgb (h, w, 3), depth (h, w))."""
+    rgb = _f32((height, width, 3))
+    depth = _f32((height, width))
+    _call(_lib().dco_render_virtual, _p(vertices), _p(triangles), _p(colors), triangles.shape[0], float(focal_px),
+          float(cx), float(cy), width, height, _p(rgb), _p(depth))
+    return rgb, depth
+
+
 # ---------------------------------------------------------------- stream ---
 class Stream:
     """One device-resident pipeline stream (pipeline.cpp:131-258 per frame)."""
@@ -449,6 +469,31 @@ class Stream:
     def set_virtual(self, virt_rgb, virt_depth):
         self._bind()
         native.check(self.ctx, self.lib.dco_stream_set_virtual(self.handle, _p(virt_rgb), _p(virt_depth)))
+
+    def set_mesh(self, vertices, triangles, colors):
+        """Virtual mesh rendered per frame (numpy arrays: (n, 3) float32
+        vertices / colours, (m, 3) int32 triangles); None clears it."""
+        self._bind()
+        if vertices is None:
+            native.check(self.ctx, self.lib.dco_stream_set_mesh(self.handle, None, 0, None, 0, None))
+            return
+        import numpy as np
+
+        v = np.ascontiguousarray(vertices, np.float32)
+        t = np.ascontiguousarray(triangles, np.int32)
+        c = np.ascontiguousarray(colors, np.float32)
+        self._mesh_keep = (v, t, c)
+        native.check(self.ctx, self.lib.dco_stream_set_mesh(
+            self.handle, ctypes.c_void_p(v.ctypes.data), len(v), ctypes.c_void_p(t.ctypes.data), len(t),
+            ctypes.c_void_p(c.ctypes.data)))
+
+    def set_next_pose(self, pose):
+        """Pose (16 doubles, row-major) of the next pushed frame; None = none."""
+        if pose is None:
+            native.check(self.ctx, self.lib.dco_stream_set_next_pose(self.handle, None))
+            return
+        p = (ctypes.c_double * 16)(*[float(x) for x in pose])
+        native.check(self.ctx, self.lib.dco_stream_set_next_pose(self.handle, ctypes.cast(p, ctypes.c_void_p)))
 
     def push_gray8(self, left8, right8, rgb8=None, want_result=True):
         self._bind()

@@ -128,9 +128,13 @@ SIGNATURES = {
     "dco_objective_value": (c_int, [c_void_p, ctypes.POINTER(System), P, ctypes.POINTER(c_double)]),
     "dco_solve_dense_depth": (c_int, [c_void_p, ctypes.POINTER(System), CFG, P, ctypes.POINTER(SolveStats)]),
     "dco_composite": (c_int, [c_void_p, P, P, P, P, c_int, c_int, P, P]),
+    "dco_transform_mesh": (c_int, [c_void_p, P, c_int, P, P]),
+    "dco_render_virtual": (c_int, [c_void_p, P, P, P, c_int, c_double, c_double, c_double, c_int, c_int, P, P]),
     "dco_stream_create": (c_int, [c_void_p, c_int, c_int, CFG, ctypes.POINTER(c_void_p)]),
     "dco_stream_destroy": (None, [c_void_p]),
     "dco_stream_set_virtual": (c_int, [c_void_p, P, P]),
+    "dco_stream_set_mesh": (c_int, [c_void_p, P, c_int, P, c_int, P]),
+    "dco_stream_set_next_pose": (c_int, [c_void_p, P]),
     "dco_stream_push_gray8": (c_int, [c_void_p, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_push_f32": (c_int, [c_void_p, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_push_gray8_host": (c_int, [c_void_p, P, P, P, P, P, ctypes.POINTER(FrameResult)]),
