@@ -9,14 +9,14 @@
 // minimum z), so every pixel must visit its covering triangles in ascending
 // index order. Here:
 //   k_tri_setup : per triangle, the reference's projection, area and clamped
-//                 bounding box (same double expressions, --fmad=false), and a
-//                 count per 16x16 tile it overlaps;
-//   k_tri_fill  : the per-tile lists (offsets from a scan of the counts);
+//                 bounding box (same double expressions, --fmad=false);
+//   k_tri_tiles : a warp per triangle counts, then fills, the 16x16 tiles it
+//                 overlaps (list offsets from a scan of the counts);
 //   k_tile_sort : each tile's list sorted ascending (bitonic, shared memory);
 //   k_raster    : one thread per pixel, walking its tile's sorted list with
 //                 the reference's barycentrics, depth test and colour.
-// Tiles whose list exceeds the shared-memory sort take k_raster_all (every
-// triangle of the mesh in order, bounding-box culled) -- exact, slower.
+// Tiles whose list exceeds the shared-memory sort walk every triangle of the
+// mesh in order instead (bounding-box culled) -- exact, slower.
 #include <math.h>
 
 #include <algorithm>
@@ -71,8 +71,7 @@ __device__ __forceinline__ double max3(double a, double b, double c) {  // std::
 
 // render_virtual, occlude.cpp:118-145: per-triangle setup + tile counts.
 __global__ void k_tri_setup(const float* __restrict__ v, const int* __restrict__ tris, const float* __restrict__ col,
-                            int nt, double focal, double cx, double cy, int w, int h, int tiles_x,
-                            TriSetup* __restrict__ ts, int* __restrict__ counts) {
+                            int nt, double focal, double cx, double cy, int w, int h, TriSetup* __restrict__ ts) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
     TriSetup s;
@@ -110,9 +109,28 @@ __global__ void k_tri_setup(const float* __restrict__ v, const int* __restrict__
         }
     }
     ts[t] = s;
+}
+
+// one warp per triangle: lanes stride over the tiles its bounding box overlaps
+// (count pass when lists == nullptr, fill pass otherwise)
+__global__ void k_tri_tiles(const TriSetup* __restrict__ ts, int nt, int tiles_x, int* __restrict__ counts,
+                            const int* __restrict__ offsets, int* __restrict__ cursor, int* __restrict__ lists, int ntiles,
+                            long long cap) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (t >= nt) return;
+    if (lists && offsets[ntiles] > cap) return;  // lists do not fit: every tile rasterises the whole mesh
+    const TriSetup& s = ts[t];
     if (s.x1 < s.x0) return;
-    for (int ty = s.y0 / kTile; ty <= s.y1 / kTile; ++ty)
-        for (int tx = s.x0 / kTile; tx <= s.x1 / kTile; ++tx) atomicAdd(counts + ty * tiles_x + tx, 1);
+    const int tx0 = s.x0 / kTile, ty0 = s.y0 / kTile;
+    const int ntx = s.x1 / kTile - tx0 + 1, nty = s.y1 / kTile - ty0 + 1;
+    for (int k = lane; k < ntx * nty; k += 32) {
+        const int tile = (ty0 + k / ntx) * tiles_x + tx0 + k % ntx;
+        if (lists) {
+            lists[offsets[tile] + atomicAdd(cursor + tile, 1)] = t;
+        } else {
+            atomicAdd(counts + tile, 1);
+        }
+    }
 }
 
 // exclusive scan of the tile counts (one block; tile counts are small)
@@ -156,23 +174,9 @@ __global__ void k_tile_scan(const int* __restrict__ counts, int n, int* __restri
     if (threadIdx.x == 0) offsets[n] = carry;
 }
 
-__global__ void k_tri_fill(const TriSetup* __restrict__ ts, int nt, int tiles_x, const int* __restrict__ offsets,
-                           int* __restrict__ cursor, int* __restrict__ lists, int ntiles, long long cap) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nt) return;
-    if (offsets[ntiles] > cap) return;  // lists do not fit: every tile rasterises the whole mesh
-    const TriSetup& s = ts[t];
-    if (s.x1 < s.x0) return;
-    for (int ty = s.y0 / kTile; ty <= s.y1 / kTile; ++ty)
-        for (int tx = s.x0 / kTile; tx <= s.x1 / kTile; ++tx) {
-            const int tile = ty * tiles_x + tx;
-            lists[offsets[tile] + atomicAdd(cursor + tile, 1)] = t;
-        }
-}
-
 // ascending sort of one tile's list (bitonic in shared memory); longer lists
 // are left unsorted and their tiles flagged for k_raster_all
-__global__ void __launch_bounds__(512) k_tile_sort(const int* __restrict__ offsets, int* __restrict__ lists,
+__global__ void __launch_bounds__(256) k_tile_sort(const int* __restrict__ offsets, int* __restrict__ lists,
                                                    int* __restrict__ overflow, int ntiles, long long cap) {
     __shared__ int key[kSortCap];
     const int tile = blockIdx.x;
@@ -230,45 +234,31 @@ __device__ __forceinline__ void shade(const TriSetup& s, int x, int y, float& de
 
 // one block per 16x16 tile: the tile's sorted list, staged through shared
 // memory in batches
-__global__ void __launch_bounds__(kTile* kTile) k_raster(const TriSetup* __restrict__ ts, const int* __restrict__ offsets,
-                                                         const int* __restrict__ lists, const int* __restrict__ overflow,
-                                                         int w, int h, int tiles_x, float* __restrict__ rgb_out,
-                                                         float* __restrict__ depth_out) {
+__global__ void __launch_bounds__(kTile* kTile) k_raster(const TriSetup* __restrict__ ts, int nt,
+                                                         const int* __restrict__ offsets, const int* __restrict__ lists,
+                                                         const int* __restrict__ overflow, int w, int h, int tiles_x,
+                                                         float* __restrict__ rgb_out, float* __restrict__ depth_out) {
     constexpr int kBatch = 64;
     __shared__ TriSetup st[kBatch];
     const int tile = blockIdx.x;
-    if (overflow[tile]) return;  // k_raster_all owns this tile
     const int x = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
     const int y = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
     float depth = __int_as_float(0x7fc00000);  // nodata
     float rgb[3] = {0.0f, 0.0f, 0.0f};
-    const int b = offsets[tile], e = offsets[tile + 1];
-    for (int k0 = b; k0 < e; k0 += kBatch) {
-        const int cnt = min(kBatch, e - k0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) st[i] = ts[lists[k0 + i]];
-        __syncthreads();
-        for (int i = 0; i < cnt; ++i) shade(st[i], x, y, depth, rgb);
+    if (overflow[tile]) {
+        // list too long for the sort (or lists did not fit): every triangle of
+        // the mesh in index order, bounding-box culled -- exact, slower
+        for (int t = 0; t < nt; ++t) shade(ts[t], x, y, depth, rgb);
+    } else {
+        const int b = offsets[tile], e = offsets[tile + 1];
+        for (int k0 = b; k0 < e; k0 += kBatch) {
+            const int cnt = min(kBatch, e - k0);
+            __syncthreads();
+            for (int i = threadIdx.x; i < cnt; i += blockDim.x) st[i] = ts[lists[k0 + i]];
+            __syncthreads();
+            for (int i = 0; i < cnt; ++i) shade(st[i], x, y, depth, rgb);
+        }
     }
-    if (x < w && y < h) {
-        const size_t p = static_cast<size_t>(y) * w + x;
-        depth_out[p] = depth;
-        rgb_out[3 * p + 0] = rgb[0];
-        rgb_out[3 * p + 1] = rgb[1];
-        rgb_out[3 * p + 2] = rgb[2];
-    }
-}
-
-// overflowed tiles: every triangle of the mesh, in order
-__global__ void k_raster_all(const TriSetup* __restrict__ ts, int nt, const int* __restrict__ overflow, int w, int h,
-                             int tiles_x, float* __restrict__ rgb_out, float* __restrict__ depth_out) {
-    const int tile = blockIdx.x;
-    if (!overflow[tile]) return;
-    const int x = (tile % tiles_x) * kTile + (threadIdx.x & (kTile - 1));
-    const int y = (tile / tiles_x) * kTile + (threadIdx.x / kTile);
-    float depth = __int_as_float(0x7fc00000);
-    float rgb[3] = {0.0f, 0.0f, 0.0f};
-    for (int t = 0; t < nt; ++t) shade(ts[t], x, y, depth, rgb);
     if (x < w && y < h) {
         const size_t p = static_cast<size_t>(y) * w + x;
         depth_out[p] = depth;
@@ -310,8 +300,11 @@ void render_virtual(dco_ctx* ctx, const float* verts, const int* tris, const flo
     cuda_check(cudaMemsetAsync(overflow, 0, static_cast<size_t>(ntiles) * 4, ctx->stream), "memset");
     if (nt > 0) {
         k_tri_setup<<<blocks_for(static_cast<size_t>(nt), 128), 128, 0, ctx->stream>>>(
-            verts, tris, colors, nt, focal_px, cx, cy, w, h, tiles_x, ts, counts);
+            verts, tris, colors, nt, focal_px, cx, cy, w, h, ts);
         launched(ctx, "k_tri_setup");
+        k_tri_tiles<<<blocks_for(static_cast<size_t>(nt) * 32, 256), 256, 0, ctx->stream>>>(
+            ts, nt, tiles_x, counts, nullptr, nullptr, nullptr, ntiles, 0);
+        launched(ctx, "k_tri_tiles");
     }
     k_tile_scan<<<1, 1024, 0, ctx->stream>>>(counts, ntiles, offsets, cursor);
     launched(ctx, "k_tile_scan");
@@ -322,16 +315,14 @@ void render_virtual(dco_ctx* ctx, const float* verts, const int* tris, const flo
                                               std::max<long long>(256LL * nt, 1 << 20));
     int* lists = static_cast<int*>(scratch(ctx, S_RENDER_LIST, static_cast<size_t>(std::max<long long>(cap, 1)) * 4));
     if (nt > 0) {
-        k_tri_fill<<<blocks_for(static_cast<size_t>(nt), 128), 128, 0, ctx->stream>>>(ts, nt, tiles_x, offsets, cursor,
-                                                                                      lists, ntiles, cap);
-        launched(ctx, "k_tri_fill");
-        k_tile_sort<<<ntiles, 512, 0, ctx->stream>>>(offsets, lists, overflow, ntiles, cap);
+        k_tri_tiles<<<blocks_for(static_cast<size_t>(nt) * 32, 256), 256, 0, ctx->stream>>>(
+            ts, nt, tiles_x, nullptr, offsets, cursor, lists, ntiles, cap);
+        launched(ctx, "k_tri_tiles");
+        k_tile_sort<<<ntiles, 256, 0, ctx->stream>>>(offsets, lists, overflow, ntiles, cap);
         launched(ctx, "k_tile_sort");
     }
-    k_raster<<<ntiles, kTile * kTile, 0, ctx->stream>>>(ts, offsets, lists, overflow, w, h, tiles_x, rgb, depth);
+    k_raster<<<ntiles, kTile * kTile, 0, ctx->stream>>>(ts, nt, offsets, lists, overflow, w, h, tiles_x, rgb, depth);
     launched(ctx, "k_raster");
-    k_raster_all<<<ntiles, kTile * kTile, 0, ctx->stream>>>(ts, nt, overflow, w, h, tiles_x, rgb, depth);
-    launched(ctx, "k_raster_all");
 }
 
 }  // namespace dco_gpu
