@@ -425,6 +425,49 @@ DenseDepthMap solve_dense_depth(const ConstraintSystem& sys, const PipelineConfi
 }
 
 // -------------------------------------------------------------- composite
+// transform_mesh / render_virtual, occlude.cpp:78-169 (dco_transform_mesh,
+// dco_render_virtual; the renderer is bit-exact with the index-ordered z-buffer)
+TriangleMesh transform_mesh(const TriangleMesh& mesh, const std::array<double, 16>& pose) {
+    const int nv = static_cast<int>(mesh.vertices.size());
+    std::vector<float> flat(3 * static_cast<size_t>(nv));
+    for (int i = 0; i < nv; ++i)
+        for (int k = 0; k < 3; ++k) flat[3 * i + k] = mesh.vertices[i][k];
+    Dev<float> v(flat), o(flat.size());
+    check(dco_transform_mesh(ctx(), v.p, nv, pose.data(), o.p));
+    o.get(flat);
+    TriangleMesh out = mesh;
+    for (int i = 0; i < nv; ++i)
+        for (int k = 0; k < 3; ++k) out.vertices[i][k] = flat[3 * i + k];
+    return out;
+}
+
+VirtualLayer render_virtual(const TriangleMesh& mesh, double focal_px, double cx, double cy, int out_width,
+                            int out_height) {
+    if (out_width < 1 || out_height < 1) throw InputError("render_virtual: output dimensions must be positive");
+    const size_t nv = mesh.vertices.size(), nt = mesh.triangles.size();
+    std::vector<float> fv(3 * nv), fc(3 * nv);
+    std::vector<int> ft(3 * nt);
+    for (size_t i = 0; i < nv; ++i)
+        for (int k = 0; k < 3; ++k) {
+            fv[3 * i + k] = mesh.vertices[i][k];
+            fc[3 * i + k] = mesh.colors[i][k];
+        }
+    for (size_t t = 0; t < nt; ++t)
+        for (int k = 0; k < 3; ++k) ft[3 * t + k] = mesh.triangles[t][k];
+    Dev<float> v(fv), c(fc);
+    Dev<int> tr(ft);
+    const size_t n = static_cast<size_t>(out_width) * out_height;
+    Dev<float> rgb(3 * n), depth(n);
+    check(dco_render_virtual(ctx(), v.p, tr.p, c.p, static_cast<int>(nt), focal_px, cx, cy, out_width, out_height,
+                             rgb.p, depth.p));
+    VirtualLayer layer;
+    layer.color = ColorImage(out_width, out_height);
+    layer.depth = FloatMap(out_width, out_height);
+    rgb.get(layer.color.data);
+    depth.get(layer.depth.data);
+    return layer;
+}
+
 CompositeResult composite(const ColorImage& real, const DenseDepthMap& dense, const VirtualLayer& virt) {
     const int w = real.width, h = real.height;
     if (dense.width != w || dense.height != h || virt.color.width != w || virt.color.height != h ||

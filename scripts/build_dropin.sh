@@ -13,9 +13,14 @@ mkdir -p "$OUT"
 make -s -C "$ROOT/oracle" ref >/dev/null
 [ -f "$ROOT/paper_2203_02300_b200/libdco_gpu.so" ] || python "$ROOT/paper_2203_02300_b200/build.py"
 OBJ=$ROOT/oracle/_ref/obj
-# occlude.o provides render_virtual/load_obj/...; its composite() yields to ours
-SYM=$(nm "$OBJ/occlude.o" | awk '/ T _ZN3dco9composite/{print $3}')
-objcopy --weaken-symbol="$SYM" "$OBJ/occlude.o" "$OUT/occlude_weak.o"
+# occlude.o provides load_obj/save_obj/make_cube_mesh; its composite(),
+# render_virtual() and transform_mesh() yield to ours
+WEAK=""
+for pat in _ZN3dco9composite _ZN3dco14render_virtual _ZN3dco14transform_mesh; do
+    SYM=$(nm "$OBJ/occlude.o" | awk -v p="$pat" '$2 == "T" && index($3, p) == 1 {print $3}')
+    WEAK="$WEAK --weaken-symbol=$SYM"
+done
+objcopy $WEAK "$OBJ/occlude.o" "$OUT/occlude_weak.o"
 FLAGS="-std=gnu++20 -O2 -DNDEBUG -w"
 $CXX $FLAGS -I"$REF/include" -I"$ROOT/include" -I"$CUDA/include" -c "$ROOT/paper_2203_02300_b200/shim/dco_dropin.cpp" -o "$OUT/dco_dropin.o"
 cp "$ROOT/paper_2203_02300_b200/libdco_gpu.so" "$OUT/"
