@@ -355,216 +355,6 @@ struct CGArgs {
     long long* dbg;  // optional per-phase clock64 stamps of block 0 (DCO_PCG_DEBUG)
 };
 
-// Sum of the per-block partials, identical in every block (same order).
-template <int K>
-__device__ __forceinline__ void grid_total(const double* part, int nb, double (&v)[K], double* sm) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = 0.0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x)
-#pragma unroll
-        for (int k = 0; k < K; ++k) v[k] += part[4 * b + k];
-    block_sum<K>(v, sm);
-}
-
-__global__ void __launch_bounds__(512) k_pcg(CGArgs a) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double sm[32 * 4];
-    const int w = a.w, h = a.h;
-    const size_t n = a.n;
-    const size_t T = static_cast<size_t>(gridDim.x) * blockDim.x;
-    const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int nb = gridDim.x;
-    double* part = a.part + 4 * blockIdx.x;
-
-    unsigned long long anchors = a.anchors_dev ? *a.anchors_dev : a.anchors_host;
-    if (anchors == 0) {  // densify.cpp:143-144 -> caller's Unsolvable handling
-        const float* fb = (a.fallback && (!a.fallback_valid || *a.fallback_valid)) ? a.fallback : nullptr;
-        for (size_t i = t0; i < n; i += T) a.dense[i] = fb ? fb[i] : __int_as_float(0x7fc00000);
-        if (t0 == 0) {
-            a.out->status = 3;
-            a.out->iterations = 0;
-        }
-        return;
-    }
-    const double cterm = a.constant_term_dev ? *a.constant_term_dev : a.constant_term_host;
-
-    // setup: x = initial, precond, r = b - A x, norms, objective(initial)
-    for (size_t i = t0; i < n; i += T) {
-        double d = a.diag[i];
-        a.prec[i] = d > 0.0 ? 1.0 / d : 1.0;
-        a.x[i] = a.init[i];
-    }
-    grid.sync();
-    {
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
-        for (size_t i = t0; i < n; i += T) {
-            int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
-            double ax = apply_at(a.diag, a.ch, a.cv, a.x, w, h, i, xx, y);
-            double b = a.rhs[i];
-            double ri = b - ax;
-            double zi = a.prec[i] * ri;
-            a.r[i] = ri;
-            a.rs[i] = ri;
-            a.xs[i] = a.x[i];
-            a.z[i] = zi;
-            a.p[i] = zi;
-            v[0] += b * b;
-            v[1] += ri * ri;
-            v[2] += ri * zi;
-        }
-        block_sum<4>(v, sm);
-        if (threadIdx.x == 0)
-            for (int k = 0; k < 4; ++k) part[k] = v[k];
-    }
-    grid.sync();
-    double tot[4];
-    grid_total<4>(a.part, nb, tot, sm);
-    const double bnorm = sqrt(tot[0]);
-    const double denom = bnorm > 0.0 ? bnorm : 1.0;
-    double snorm = sqrt(tot[1]);
-    double rho = tot[2];
-    if (t0 == 0) {
-        if (a.hist_cap > 0) a.hist[0] = snorm;
-    }
-    grid.sync();  // everyone has read the setup partials
-    // objective(initial) = dot(x,Ax) - 2 dot(b,x) + c, as two separate tree sums
-    {
-        double v[2] = {0.0, 0.0};
-        for (size_t i = t0; i < n; i += T) {
-            int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
-            v[0] += a.x[i] * apply_at(a.diag, a.ch, a.cv, a.x, w, h, i, xx, y);
-            v[1] += a.rhs[i] * a.x[i];
-        }
-        block_sum<2>(v, sm);
-        if (threadIdx.x == 0) {
-            part[0] = v[0];
-            part[1] = v[1];
-        }
-    }
-    grid.sync();
-    {
-        double o[2];
-        grid_total<2>(a.part, nb, o, sm);
-        if (t0 == 0) a.out->objective_initial = o[0] - 2.0 * o[1] + cterm;
-    }
-    grid.sync();
-
-    int iter = 0;
-    while (iter < a.max_iter && snorm / denom > a.tol) {
-        // phase A: q = A p, pq
-        {
-            double v[1] = {0.0};
-            for (size_t i = t0; i < n; i += T) {
-                int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
-                double qi = apply_at(a.diag, a.ch, a.cv, a.p, w, h, i, xx, y);
-                a.q[i] = qi;
-                v[0] += a.p[i] * qi;
-            }
-            block_sum<1>(v, sm);
-            if (threadIdx.x == 0) part[0] = v[0];
-        }
-        grid.sync();
-        double pq;
-        {
-            double t[1];
-            grid_total<1>(a.part, nb, t, sm);
-            pq = t[0];
-        }
-        if (pq <= 0.0) break;  // uniform across the grid
-        const double alpha = rho / pq;
-        grid.sync();  // partials consumed before they are overwritten
-        // phase B: x, r, z; rho_next; MR numerators
-        {
-            double v[3] = {0.0, 0.0, 0.0};
-            for (size_t i = t0; i < n; i += T) {
-                double xi = a.x[i] + alpha * a.p[i];
-                double ri = a.r[i] - alpha * a.q[i];
-                double zi = a.prec[i] * ri;
-                a.x[i] = xi;
-                a.r[i] = ri;
-                a.z[i] = zi;
-                v[0] += ri * zi;
-                double rsi = a.rs[i];
-                double di = ri - rsi;
-                v[1] += rsi * di;
-                v[2] += di * di;
-            }
-            block_sum<3>(v, sm);
-            if (threadIdx.x == 0)
-                for (int k = 0; k < 3; ++k) part[k] = v[k];
-        }
-        grid.sync();
-        double rho_next, sd, dd;
-        {
-            double t[3];
-            grid_total<3>(a.part, nb, t, sm);
-            rho_next = t[0];
-            sd = t[1];
-            dd = t[2];
-        }
-        const double beta = rho_next / rho;
-        rho = rho_next;
-        double eta = 0.0;
-        if (dd > 0.0) {
-            eta = -sd / dd;
-            eta = eta < 0.0 ? 0.0 : (1.0 < eta ? 1.0 : eta);  // std::clamp(., 0, 1)
-        }
-        grid.sync();
-        // phase C: p update, MR smoothing, |rs|^2
-        {
-            double v[1] = {0.0};
-            for (size_t i = t0; i < n; i += T) {
-                a.p[i] = a.z[i] + beta * a.p[i];
-                double rsi = a.rs[i];
-                if (eta > 0.0) {
-                    rsi += eta * (a.r[i] - rsi);
-                    a.rs[i] = rsi;
-                    double xsi = a.xs[i];
-                    a.xs[i] = xsi + eta * (a.x[i] - xsi);
-                }
-                v[0] += rsi * rsi;
-            }
-            block_sum<1>(v, sm);
-            if (threadIdx.x == 0) part[0] = v[0];
-        }
-        grid.sync();
-        {
-            double t[1];
-            grid_total<1>(a.part, nb, t, sm);
-            snorm = sqrt(t[0]);
-        }
-        ++iter;
-        if (t0 == 0 && iter < a.hist_cap) a.hist[iter] = snorm;
-        grid.sync();
-    }
-    // objective(xs) and the dense map
-    {
-        double v[2] = {0.0, 0.0};
-        for (size_t i = t0; i < n; i += T) {
-            int xx = static_cast<int>(i % w), y = static_cast<int>(i / w);
-            double xsi = a.xs[i];
-            v[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
-            v[1] += a.rhs[i] * xsi;
-            a.dense[i] = static_cast<float>(dmax0(xsi));
-        }
-        block_sum<2>(v, sm);
-        if (threadIdx.x == 0) {
-            part[0] = v[0];
-            part[1] = v[1];
-        }
-    }
-    grid.sync();
-    {
-        double o[2];
-        grid_total<2>(a.part, nb, o, sm);
-        if (t0 == 0) {
-            a.out->objective_final = o[0] - 2.0 * o[1] + cterm;
-            a.out->status = 0;
-            a.out->iterations = iter;
-            a.out->relative_residual = snorm / denom;
-        }
-    }
-}
 
 // ------------------------------------------------- on-chip resident solver --
 // Same Krylov iterates as k_pcg, but each of the grid's blocks (one per SM,
@@ -879,13 +669,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
 
 #include "pcg_tmem.cuh"
 #include "pcg_big.cuh"
+#include "pcg_stream.cuh"
 
 namespace dco_gpu {
 namespace {
 
 inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
 
-int g_pcg_blocks = 0;
 long long* g_pcg_dbg = nullptr;
 constexpr int kDbgLen = 1280 + 64 * 1024 * 3;  // + per-block globaltimer stamps
 int g_sms = 0;
@@ -1034,14 +824,6 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
                      void* out_dev) {
     const int w = sys->width, h = sys->height;
     const size_t n = static_cast<size_t>(w) * h;
-    if (!g_pcg_blocks) {
-        int dev = ctx->device, sms = 0, per = 0;
-        cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pcg, 512, 0), "occupancy");
-        require(per >= 1, "solve_dense_depth: solver kernel does not fit an SM");
-        g_pcg_blocks = sms * std::min(per, 2);
-    }
-    const int nb = g_pcg_blocks;
     double* wk = static_cast<double*>(scratch(ctx, S_CG, (8 * n + 48 * 1024 + 64) * sizeof(double)));
     CGArgs a;
     a.w = w;
@@ -1092,8 +874,10 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     // the registers + shared-memory variant
     const bool no_tmem = getenv("DCO_PCG_NO_TMEM") != nullptr;
     OnchipKernel kern = no_tmem ? onchip_for(threads, ept) : tmem_for(ept);
-    // DCO_PCG_FORCE_BIG=1 (tests): the large-frame kernel even when the state fits on chip
-    const bool force_big = getenv("DCO_PCG_FORCE_BIG") != nullptr;
+    // DCO_PCG_FORCE_BIG=1 / DCO_PCG_FORCE_STREAM=1 (tests): the large-frame /
+    // any-size kernel even when the state fits on chip
+    const bool force_stream = getenv("DCO_PCG_FORCE_STREAM") != nullptr;
+    const bool force_big = force_stream || getenv("DCO_PCG_FORCE_BIG") != nullptr;
     // DCO_PCG_SHARE=1: the co-residency variant (512 threads, p-only shared memory)
     if (getenv("DCO_PCG_SHARE") && sms <= 1024) {
         const int ept_s = std::max(9, (chunk + kShareThreads - 1) / kShareThreads);
@@ -1142,7 +926,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         const int ept_b = (chunk + kBigThreads - 1) / kBigThreads;
         const size_t smem_b = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
         BigKernel bk = big_for(ept_b < 9 ? 9 : ept_b);
-        if (bk && smem_b <= kOnchipSmemMax && sms <= 1024 && !getenv("DCO_PCG_NO_BIG")) {
+        if (bk && !force_stream && smem_b <= kOnchipSmemMax && sms <= 1024 && !getenv("DCO_PCG_NO_BIG")) {
             static int attr_b[22] = {};
             const int e = ept_b < 9 ? 9 : ept_b;
             if (attr_b[e] < static_cast<int>(smem_b)) {
@@ -1162,9 +946,28 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
             return;
         }
     }
-    void* params[] = {&a};
-    launch_cooperative_serialized(ctx, reinterpret_cast<void*>(k_pcg), dim3(nb), dim3(512), params, 0);
-    launched(ctx, "k_pcg");
+    // any size: every vector in global memory, one grid barrier per iteration
+    {
+        StreamVecs sv;
+        double* sb = static_cast<double*>(scratch(ctx, S_TMP1, 6 * n * sizeof(double)));
+        for (int k = 0; k < 2; ++k) {
+            sv.p[k] = sb + (0 + k) * n;
+            sv.r[k] = sb + (2 + k) * n;
+            sv.q[k] = sb + (4 + k) * n;
+        }
+        sv.x = a.x;
+        sv.xs = a.xs;
+        sv.rs = a.rs;
+        GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
+        cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
+        void* params[] = {&a, &sv, &bar};
+        // 512 threads x 2 batched elements: 16.7 ms at 3840x2160 (768 x 1 the
+        // same; 1024 x 1 18.3, 384 x 2 18.0, 256 x 4 19.4, 512 x 3 spills)
+        void* fn = reinterpret_cast<void*>(k_pcg_stream<512, 2>);
+        const int threads = 512;
+        launch_cooperative_serialized(ctx, fn, dim3(sms), dim3(threads), params, 0);
+        launched(ctx, "k_pcg_stream");
+    }
 }
 
 size_t solve_out_bytes() { return sizeof(SolveOut); }

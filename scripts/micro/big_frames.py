@@ -12,7 +12,10 @@ from paper_2203_02300_b200 import dco  # noqa: E402
 from paper_2203_02300_b200.config import Config  # noqa: E402
 from paper_2203_02300_b200.synth import StereoVideo  # noqa: E402
 
-for W, H, D in ((1920, 1080, 192), (3840, 2160, 256)):
+SIZES = ((1920, 1080, 192), (3840, 2160, 256))
+if len(sys.argv) > 1:  # e.g. 3840x2160
+    SIZES = [z for z in SIZES if "%dx%d" % z[:2] in sys.argv[1:]]
+for W, H, D in SIZES:
     cfg = Config(d_max=D - 1)
     vid = StereoVideo(W, H)
     frames = [vid.frame(i) for i in range(6)]

@@ -71,15 +71,17 @@ def _solve_both(gpu, ref, sparse, edges, m_fuse, m_i, pre, cfg):
     return N(got), gst, want, st
 
 
-VARIANT_ENV = {"tmem": None, "onchip": "DCO_PCG_NO_TMEM", "big": "DCO_PCG_FORCE_BIG", "share": "DCO_PCG_SHARE"}
+VARIANT_ENV = {"tmem": None, "onchip": "DCO_PCG_NO_TMEM", "big": "DCO_PCG_FORCE_BIG", "share": "DCO_PCG_SHARE",
+               "stream": "DCO_PCG_FORCE_STREAM"}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANT_ENV))
 @pytest.mark.parametrize("seed,with_pre", [(5150, False), (5151, True), (77, False)])
 def test_solve_small_within_tolerance(gpu, ref, seed, with_pre, variant, monkeypatch):
     """Every solver variant: tmem (default), onchip (registers + shared memory,
-    DCO_PCG_NO_TMEM), big (x/xs/coefficients in L2, forced on a small system)
-    and share (the co-residency kernel)."""
+    DCO_PCG_NO_TMEM), big (x/xs/coefficients in L2, forced on a small system),
+    share (the co-residency kernel) and stream (every vector in global memory,
+    the any-size path)."""
     if VARIANT_ENV[variant]:
         monkeypatch.setenv(VARIANT_ENV[variant], "1")
     cfg = Config(solver_tol=1e-12, solver_max_iter=3000)
