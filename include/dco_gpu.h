@@ -34,7 +34,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define DCO_ABI_VERSION 2
+#define DCO_ABI_VERSION 3
 
 typedef enum dco_status {
     DCO_OK = 0,
@@ -314,6 +314,35 @@ int dco_stream_span_times(dco_stream* s, double* ms, uint64_t* frames);
 size_t dco_stream_state_size(const dco_stream* s);
 int dco_stream_save_state(dco_stream* s, void* host_buf, size_t len);
 int dco_stream_load_state(dco_stream* s, const void* host_buf, size_t len);
+
+/* ---- row bands (3840x2160 over G GPUs) ------------
+ * The quarter-scale rows split into G contiguous bands. Band k computes the
+ * stereo chain on its rows plus a recompute halo of (I+1)*l1 + max(Rc,1)
+ * rows each side (I = hist_iterations, Rc = census half-height), so every
+ * owned row is bit-equal to the whole frame's. The one true exchange is the
+ * aggregation's sequential column prefix (stereo.cpp:203-215): band k starts
+ * it at carry_row from band k-1's exact prefix (qw * nd doubles, [x][d]) and
+ * exports its prefix at carry_out_row to band k+1 -- a chain over bands. No
+ * reference function is replaced; this is the multi-GPU split of
+ * dco_stereo_sparse_depth (pipeline.cpp:184-195). */
+typedef struct dco_band {
+    int row0, row1;       /* owned quarter rows [row0, row1)                      */
+    int sub0, sub1;       /* quarter rows computed: owned + halo, clipped          */
+    int carry_row;        /* quarter row the prefix arrives at; 0 = no carry in     */
+    int carry_out_row;    /* row whose prefix goes to band k+1; -1 = none           */
+    int frow0, frow1;     /* full-resolution rows of the band's sparse depth        */
+    int halo;             /* recompute halo in quarter rows                        */
+} dco_band;
+int dco_band_plan(const dco_config* cfg, int full_w, int full_h, int bands, int index, dco_band* out);
+/* Bytes of one carry buffer: (full_w / 2) * (d_max - d_min + 1) doubles. */
+size_t dco_band_carry_bytes(const dco_config* cfg, int full_w);
+/* Stereo chain of one band. left_sub / right_sub: quarter rows [sub0, sub1)
+ * (qw = full_w / 2 wide). carry_in: required when carry_row > 0; carry_out:
+ * written when carry_out_row >= 0. disparity: (row1-row0)*qw, may be NULL;
+ * sparse: full rows [frow0, frow1) of full_w. */
+int dco_stereo_band(dco_ctx* ctx, const float* left_sub, const float* right_sub, const dco_band* band,
+                    const dco_config* cfg, int full_w, int full_h, const double* carry_in, double* carry_out,
+                    float* disparity, float* sparse);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

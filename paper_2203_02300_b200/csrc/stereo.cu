@@ -539,10 +539,17 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_h2(const float* __restrict_
 
 // Pipelined vertical pass: same chain, rounding and division as k_agg_vpass.
 // Block = 32 slices x 4 columns.
-template <int kPF>
+// kBand (row bands, DESIGN 7): the column prefix starts at row c0 from the
+// exact prefix of the rows above the band (carry_in, [x][d] doubles, or 0)
+// -- rows < c0 add nothing -- and the prefix before row e is exported to
+// carry_out for the next band. Same chain, so the exact rows are bit-equal to
+// the whole frame's.
+template <int kPF, bool kBand = false>
 __global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict__ hsum, int w, int h, int nd,
                                                         const uint32_t* __restrict__ vinfo, int lag, int ring_n,
-                                                        float* __restrict__ out) {
+                                                        float* __restrict__ out, const double* __restrict__ carry_in = nullptr,
+                                                        int c0 = 0, double* __restrict__ carry_out = nullptr,
+                                                        int e = -1) {
     extern __shared__ double ring[];
     const int lane = threadIdx.x, tid = threadIdx.y * 32 + threadIdx.x;
     const int k = blockIdx.x * 32 + lane;
@@ -554,13 +561,18 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict
     const uint32_t* info = vinfo + x;
     double* rg = ring + tid;
     double C = 0.0;
-    rg[0] = 0.0;
+    if (kBand && carry_in) C = carry_in[static_cast<size_t>(x) * nd + k];
+    rg[0] = C;
     int s1 = 0;
+    auto note = [&](int y) {  // C is now the prefix before row y + 1
+        if (kBand && y + 1 == e) carry_out[static_cast<size_t>(x) * nd + k] = C;
+    };
+    auto live = [&](int y) { return !kBand || y >= c0; };
     double cur[kPF], nxt[kPF];
     uint32_t ci[kPF], ni[kPF];
 #pragma unroll
     for (int j = 0; j < kPF; ++j) {
-        cur[j] = j < h ? __ldg(lp) : 0.0;
+        cur[j] = (j < h && live(j)) ? __ldg(lp) : 0.0;
         lp += row;
         const int py = j + 1 - lag;
         ci[j] = (py >= 0 && py < h) ? __ldg(info + static_cast<size_t>(py) * w) : 0u;
@@ -583,7 +595,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict
             const uint32_t* ip = info + static_cast<size_t>(y0 + kPF + 1 - lag) * w;
 #pragma unroll
             for (int j = 0; j < kPF; ++j) {
-                nxt[j] = __ldg(lp);
+                nxt[j] = live(y0 + kPF + j) ? __ldg(lp) : 0.0;
                 lp += row;
                 ni[j] = __ldg(ip);
                 ip += w;
@@ -596,6 +608,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict
                 C += cur[j];
                 s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
                 rg[s1 * kAggThreads] = C;
+                note(y0 + j);
             }
             float* dp = dst + static_cast<size_t>(y0 + 1 - lag) * row;
             int sj = sb;
@@ -616,7 +629,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict
 #pragma unroll
             for (int j = 0; j < kPF; ++j) {
                 const int y = y0 + kPF + j;
-                nxt[j] = y < h ? __ldg(lp) : 0.0;
+                nxt[j] = (y < h && live(y)) ? __ldg(lp) : 0.0;
                 lp += row;
                 const int py = y + 1 - lag;
                 ni[j] = (py >= 0 && py < h) ? __ldg(info + static_cast<size_t>(py) * w) : 0u;
@@ -633,6 +646,7 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict
                         s1 = (s1 + 1 == ring_n) ? 0 : s1 + 1;
                         rg[s1 * kAggThreads] = C;
                     }
+                    note(y);
                 }
             }
         }
@@ -1477,6 +1491,42 @@ void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, in
     k_cost_volume<<<grid, dim3(32, 16), 0, ctx->stream>>>(left, right, census, census + n, l, r, u, d, hp,
                                                            cost);
     launched(ctx, "k_cost_volume");
+}
+
+// A row band's aggregation (DESIGN 7): the packed passes with the vertical
+// prefix seeded from the band above and exported to the band below.
+void aggregate_costs_band(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l,
+                          const uint8_t* r, const uint8_t* u, const uint8_t* d, int max_arm, float* out,
+                          const double* carry_in, int c0, double* carry_out, int e) {
+    require(nd >= 1, "aggregate_costs: empty disparity range");
+    require(max_arm >= 0 && max_arm <= 127, "row bands: cross_arm_l1 must be <= 127");
+    const size_t n = static_cast<size_t>(w) * h;
+    double* hsum = static_cast<double*>(scratch(ctx, S_HSUM, n * nd * sizeof(double)));
+    const int lag = max_arm + 1;
+    uint32_t* hinfo = static_cast<uint32_t*>(scratch(ctx, S_REGION, 2 * n * sizeof(uint32_t)));
+    uint32_t* vinfo = hinfo + n;
+    dim3 b(32, 8);
+    k_region_pack<<<grid2(w, h, b), b, 0, ctx->stream>>>(l, r, u, d, w, h, hinfo, vinfo);
+    launched(ctx, "k_region_pack");
+    constexpr int kVPF = 8, kHPF = 16;
+    const int ring_h = 2 * max_arm + 2 + kHPF - 1, ring_v = 2 * max_arm + 2 + kVPF - 1;
+    dim3 tb(32, 4);
+    const size_t smem_h = static_cast<size_t>(ring_h) * kAggThreads * sizeof(double);
+    const size_t smem_v = static_cast<size_t>(ring_v) * kAggThreads * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_agg_v2<kVPF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_agg_v2<kVPF, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    k_agg_h2<kHPF><<<dim3((nd + 31) / 32, (h + 3) / 4), tb, smem_h, ctx->stream>>>(cost, w, h, nd, hinfo, lag,
+                                                                                  ring_h, hsum);
+    launched(ctx, "k_agg_h2");
+    k_agg_v2<kVPF, true><<<dim3((nd + 31) / 32, (w + 3) / 4), tb, smem_v, ctx->stream>>>(
+        hsum, w, h, nd, vinfo, lag, ring_v, out, carry_in, c0, carry_out, e);
+    launched(ctx, "k_agg_v2_band");
 }
 
 void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l,

@@ -198,6 +198,44 @@ def stereo_sparse_depth(left_q, right_q, cfg: Config, full_width, full_height):
     return disp, sparse
 
 
+# ------------------------------------------------------------- row bands ---
+def band_plan(cfg: Config, full_width, full_height, bands, index):
+    """dco_band_plan: the quarter rows band `index` of `bands` owns, computes
+    (halo) and exchanges the aggregation column prefix at. Host only."""
+    b = native.Band()
+    st = native.load().dco_band_plan(ctypes.byref(cfg), full_width, full_height, bands, index, ctypes.byref(b))
+    if st != 0:
+        from .config import raise_for
+
+        raise_for(st, "dco_band_plan: invalid band request (%dx%d, %d bands, index %d)"
+                  % (full_width, full_height, bands, index))
+    return b
+
+
+def band_carry_elems(cfg: Config, full_width):
+    """Doubles in one carry buffer: (full_width // 2) * nd."""
+    return native.load().dco_band_carry_bytes(ctypes.byref(cfg), full_width) // 8
+
+
+def stereo_band(left_sub, right_sub, band, cfg: Config, full_width, full_height, carry_in=None):
+    """dco_stereo_band: the stereo chain of one row band. left_sub/right_sub are
+    the quarter rows [band.sub0, band.sub1). Returns (disparity rows
+    [row0, row1), sparse full rows [frow0, frow1), carry_out or None)."""
+    qw = full_width // 2
+    if tuple(left_sub.shape) != (band.sub1 - band.sub0, qw) or left_sub.shape != right_sub.shape:
+        raise InputError("stereo_band: sub-images must be (sub1 - sub0, full_width // 2)")
+    if carry_in is not None and (carry_in.dtype != torch.float64 or carry_in.numel() != band_carry_elems(cfg, full_width)):
+        raise InputError("stereo_band: carry_in must hold (full_width // 2) * nd doubles")
+    disp = _f32((band.row1 - band.row0, qw))
+    sparse = _f32((band.frow1 - band.frow0, full_width))
+    carry_out = None
+    if band.carry_out_row >= 0:
+        carry_out = torch.empty(band_carry_elems(cfg, full_width), dtype=torch.float64, device="cuda")
+    _call(_lib().dco_stereo_band, _p(left_sub), _p(right_sub), ctypes.byref(band), ctypes.byref(cfg),
+          full_width, full_height, _p(carry_in), _p(carry_out), _p(disp), _p(sparse))
+    return disp, sparse, carry_out
+
+
 # ------------------------------------------------------------------ flow ---
 def compute_flow(frm, to, cfg: Config):
     """compute_flow, flow.cpp:185-205: (u, v)."""

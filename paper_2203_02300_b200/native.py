@@ -81,6 +81,13 @@ class FrameViews(ctypes.Structure):
     ]
 
 
+class Band(ctypes.Structure):
+    """dco_band: one row band of a frame split over GPUs."""
+
+    _fields_ = [(n, c_int) for n in ("row0", "row1", "sub0", "sub1", "carry_row", "carry_out_row",
+                                     "frow0", "frow1", "halo")]
+
+
 CFG = ctypes.POINTER(Config)
 
 # name -> (restype, argtypes); every function of include/dco_gpu.h
@@ -130,6 +137,9 @@ SIGNATURES = {
     "dco_composite": (c_int, [c_void_p, P, P, P, P, c_int, c_int, P, P]),
     "dco_transform_mesh": (c_int, [c_void_p, P, c_int, P, P]),
     "dco_render_virtual": (c_int, [c_void_p, P, P, P, c_int, c_double, c_double, c_double, c_int, c_int, P, P]),
+    "dco_band_plan": (c_int, [CFG, c_int, c_int, c_int, c_int, ctypes.POINTER(Band)]),
+    "dco_band_carry_bytes": (c_size_t, [CFG, c_int]),
+    "dco_stereo_band": (c_int, [c_void_p, P, P, ctypes.POINTER(Band), CFG, c_int, c_int, P, P, P, P]),
     "dco_stream_create": (c_int, [c_void_p, c_int, c_int, CFG, ctypes.POINTER(c_void_p)]),
     "dco_stream_destroy": (None, [c_void_p]),
     "dco_stream_set_virtual": (c_int, [c_void_p, P, P]),
@@ -164,7 +174,7 @@ def load(path=LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.dco_abi_version() != 2:
+    if lib.dco_abi_version() != 3:
         raise RuntimeError("libdco_gpu.so ABI mismatch")
     _lib = lib
     return lib
