@@ -344,6 +344,33 @@ int dco_stereo_band(dco_ctx* ctx, const float* left_sub, const float* right_sub,
                     const dco_config* cfg, int full_w, int full_h, const double* carry_in, double* carry_out,
                     float* disparity, float* sparse);
 
+/* Row-band densify (SURVEY 8e "1-row p halo per SpMV plus an all-reduce of
+ * the scalar groups per iteration"): the PCG + MR solve of one frame's system
+ * with rank k owning full rows [row0, row0 + rows). One persistent kernel per
+ * GPU; the per-iteration reduction and the p halo cross GPUs through peer
+ * memory (CUDA IPC over NVLink), not NCCL calls between launches. The
+ * system passed to a solve is the band's: width x rows arrays starting at the
+ * band's first row, coup_v readable one row above it when row0 > 0. The
+ * Krylov scalars are the same on every rank; the result matches
+ * dco_solve_dense_depth within the solver tolerance (densify.cpp:141-222). */
+#define DCO_BAND_HANDLE_BYTES 128
+typedef struct dco_band_solver dco_band_solver;
+int dco_band_solver_create(dco_ctx* ctx, int ranks, int rank, int width, int row0, int rows, int full_height,
+                           dco_band_solver** out);
+void dco_band_solver_destroy(dco_band_solver* s);
+/* One process per GPU: export this rank's handle (DCO_BAND_HANDLE_BYTES), gather
+ * every rank's (e.g. over torch.distributed), connect with the rank-ordered table. */
+int dco_band_solver_export(dco_band_solver* s, void* handle);
+int dco_band_solver_connect(dco_band_solver* s, const void* handles);
+int dco_band_solve(dco_band_solver* s, const dco_system* sys, const dco_config* cfg, uint64_t anchors_total,
+                   double constant_total, float* dense, dco_solve_stats* stats);
+/* Every rank in this process on one context (fewer GPUs than ranks): one
+ * cooperative launch runs all ranks as block groups. sys, dense, stats: [ranks]. */
+int dco_band_solver_connect_local(dco_band_solver* const* solvers, int ranks);
+int dco_band_solve_local(dco_band_solver* const* solvers, int ranks, const dco_system* sys, const dco_config* cfg,
+                         uint64_t anchors_total, double constant_total, float* const* dense,
+                         dco_solve_stats* stats);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -670,6 +670,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_onchip(CGArgs a, int chunk, 
 #include "pcg_tmem.cuh"
 #include "pcg_big.cuh"
 #include "pcg_stream.cuh"
+#include "pcg_band.cuh"
 
 namespace dco_gpu {
 namespace {
@@ -1072,6 +1073,326 @@ int dco_objective_value(dco_ctx* ctx, const dco_system* sys, const double* x, do
         cuda_check(cudaMemcpyAsync(hp, part + 2 * nblk, 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
         cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
         *out = hp[0];
+    });
+}
+
+// ------------------------------------------------------ row-band solver ---
+// One rank's share of a system split into row bands (pcg_band.cuh): its
+// vectors, exchange table and flags in ONE device arena, so a single IPC
+// handle exports everything the peers touch.
+struct dco_band_solver {
+    dco_ctx* ctx = nullptr;
+    int ranks = 1, rank = 0, w = 0, row0 = 0, rows = 0, H = 0;
+    size_t n = 0;
+    char* arena = nullptr;
+    size_t arena_bytes = 0;
+    dco_gpu::BandRank desc{};      // host copy; completed per solve
+    dco_gpu::BandRank* desc_dev = nullptr;
+    void* peer_base[dco_gpu::kMaxBandRanks] = {};  // mapped arenas (IPC) or local ones
+    int peer_rows[dco_gpu::kMaxBandRanks] = {};
+    bool ipc_opened[dco_gpu::kMaxBandRanks] = {};
+    bool connected = false;
+    bool local = false;  // connected with dco_band_solver_connect_local
+};
+
+namespace dco_gpu {
+namespace {
+
+constexpr int kBandVecs = 10;  // p0 p1 r0 r1 q0 q1 prec x xs rs
+constexpr size_t kBandMaxBlocks = 1024;
+
+struct BandLayout {
+    size_t words, xslots, xflags, xgen, bar, out, part, total;
+};
+
+BandLayout band_layout(size_t n) {
+    BandLayout L;
+    L.words = (kBandVecs * n * sizeof(double) + 255) / 256 * 256;
+    L.xslots = L.words;
+    L.xflags = L.xslots + 2 * kMaxBandRanks * 16 * sizeof(double);
+    L.xgen = L.xflags + kMaxBandRanks * 32 * sizeof(unsigned);
+    L.bar = L.xgen + 256;
+    L.out = L.bar + (sizeof(GridBar) + 255) / 256 * 256;
+    L.part = L.out + 256;
+    L.total = L.part + 2 * 16 * kBandMaxBlocks * sizeof(double);
+    return L;
+}
+
+// The neighbour's boundary row `row` of an arena holding `n` unknowns.
+BandSide band_side(char* base, size_t n, size_t row_off) {
+    double* v = reinterpret_cast<double*>(base);
+    BandSide S;
+    for (int k = 0; k < 2; ++k) {
+        S.p[k] = v + (0 + k) * n + row_off;
+        S.r[k] = v + (2 + k) * n + row_off;
+        S.q[k] = v + (4 + k) * n + row_off;
+    }
+    S.prec = v + 6 * n + row_off;
+    S.x = v + 7 * n + row_off;
+    S.xs = v + 8 * n + row_off;
+    return S;
+}
+
+// Wires the peer pointers of s once peer_base / peer_rows are known.
+void band_wire(dco_band_solver* s) {
+    BandLayout L = band_layout(s->n);
+    BandRank& R = s->desc;
+    R.rank = s->rank;
+    R.ranks = s->ranks;
+    R.y0 = s->row0;
+    R.H = s->H;
+    double* v = reinterpret_cast<double*>(s->arena);
+    for (int k = 0; k < 2; ++k) {
+        R.sv.p[k] = v + (0 + k) * s->n;
+        R.sv.r[k] = v + (2 + k) * s->n;
+        R.sv.q[k] = v + (4 + k) * s->n;
+    }
+    R.sv.x = v + 7 * s->n;
+    R.sv.xs = v + 8 * s->n;
+    R.sv.rs = v + 9 * s->n;
+    R.bar = reinterpret_cast<GridBar*>(s->arena + L.bar);
+    R.xslots = reinterpret_cast<double*>(s->arena + L.xslots);
+    R.xflags = reinterpret_cast<unsigned*>(s->arena + L.xflags);
+    R.xgen = reinterpret_cast<unsigned*>(s->arena + L.xgen);
+    for (int r = 0; r < kMaxBandRanks; ++r) {
+        R.peer_slots[r] = nullptr;
+        R.peer_flags[r] = nullptr;
+    }
+    for (int r = 0; r < s->ranks; ++r) {
+        char* b = static_cast<char*>(s->peer_base[r]);
+        const size_t pn = static_cast<size_t>(s->w) * s->peer_rows[r];
+        BandLayout P = band_layout(pn);
+        R.peer_slots[r] = reinterpret_cast<double*>(b + P.xslots);
+        R.peer_flags[r] = reinterpret_cast<unsigned*>(b + P.xflags);
+    }
+    memset(&R.up, 0, sizeof(R.up));
+    memset(&R.dn, 0, sizeof(R.dn));
+    if (s->rank > 0) {
+        const size_t pn = static_cast<size_t>(s->w) * s->peer_rows[s->rank - 1];
+        R.up = band_side(static_cast<char*>(s->peer_base[s->rank - 1]), pn, pn - s->w);
+    }
+    if (s->rank + 1 < s->ranks) {
+        const size_t pn = static_cast<size_t>(s->w) * s->peer_rows[s->rank + 1];
+        R.dn = band_side(static_cast<char*>(s->peer_base[s->rank + 1]), pn, 0);
+    }
+    s->connected = true;
+}
+
+// Completes the per-solve fields of a rank's descriptor.
+void band_fill(dco_band_solver* s, const dco_system* sys, const dco_config* cfg, unsigned long long anchors,
+               double cterm, float* dense, double* hist, int hist_cap) {
+    require(s->connected, "band solver: not connected");
+    require(sys->width == s->w && sys->height == s->rows, "band solver: system is not this band's");
+    BandLayout L = band_layout(s->n);
+    CGArgs& a = s->desc.a;
+    memset(&a, 0, sizeof(a));
+    a.w = s->w;
+    a.h = s->rows;
+    a.n = s->n;
+    a.diag = sys->diag;
+    a.ch = sys->coup_h;
+    a.cv = sys->coup_v;
+    a.rhs = sys->rhs;
+    a.init = sys->initial;
+    a.constant_term_host = cterm;
+    a.anchors_host = anchors;
+    double* v = reinterpret_cast<double*>(s->arena);
+    a.prec = v + 6 * s->n;
+    a.x = v + 7 * s->n;
+    a.xs = v + 8 * s->n;
+    a.rs = v + 9 * s->n;
+    a.part = reinterpret_cast<double*>(s->arena + L.part);
+    a.hist = hist;
+    a.hist_cap = hist ? hist_cap : 0;
+    a.max_iter = cfg->solver_max_iter;
+    a.tol = cfg->solver_tol;
+    a.dense = dense;
+    a.out = reinterpret_cast<SolveOut*>(s->arena + L.out);
+}
+
+void band_launch(dco_ctx* ctx, dco_band_solver* const* ss, int count) {
+    const int sms = g_sms ? g_sms : (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, ctx->device), g_sms);
+    const int bpr = std::min<int>(static_cast<int>(kBandMaxBlocks), sms / count);
+    require(bpr >= 1, "band solver: more ranks on this GPU than SMs");
+    BandRank* dd = ss[0]->desc_dev;
+    for (int k = 0; k < count; ++k) {
+        BandLayout L = band_layout(ss[k]->n);
+        cuda_check(cudaMemsetAsync(ss[k]->arena + L.bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
+        cuda_check(cudaMemcpyAsync(dd + k, &ss[k]->desc, sizeof(BandRank), cudaMemcpyHostToDevice, ctx->stream),
+                   "band desc");
+    }
+    // the descriptors are read by the kernel; keep the host copies stable until it has them
+    cuda_check(cudaStreamSynchronize(ctx->stream), "band desc sync");
+    int bpr_arg = bpr;
+    void* params[] = {&dd, &bpr_arg};
+    launch_cooperative_serialized(ctx, reinterpret_cast<void*>(k_pcg_band<kBandThreads, kBandB>),
+                                  dim3(bpr * count), dim3(kBandThreads), params, 0);
+    launched(ctx, "k_pcg_band");
+}
+
+void band_stats(dco_ctx* ctx, dco_band_solver* s, dco_solve_stats* stats, double* hist) {
+    BandLayout L = band_layout(s->n);
+    void* hp = pinned_host(ctx, 256);
+    cuda_check(cudaMemcpyAsync(hp, s->arena + L.out, solve_out_bytes(), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+    int status, iters;
+    double rr, o0, o1;
+    read_solve_out(hp, &status, &iters, &rr, &o0, &o1);
+    if (status == 3) fail(DCO_UNSOLVABLE, "solve_dense_depth: no pixel carries a data or stability constraint");
+    if (stats) {
+        stats->iterations = iters;
+        stats->relative_residual = rr;
+        stats->objective_initial = o0;
+        stats->objective_final = o1;
+        if (hist && stats->history_cap > 0) {
+            const int m = std::min(stats->history_cap, iters + 1);
+            cuda_check(cudaMemcpy(stats->history, hist, m * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+        }
+    }
+}
+
+struct IpcBlob {
+    cudaIpcMemHandle_t handle;
+    int rows, w, rank, magic;
+};
+static_assert(sizeof(IpcBlob) <= 128, "DCO_BAND_HANDLE_BYTES");
+
+}  // namespace
+}  // namespace dco_gpu
+
+int dco_band_solver_create(dco_ctx* ctx, int ranks, int rank, int width, int row0, int rows, int full_height,
+                           dco_band_solver** out) {
+    return guarded(ctx, [&] {
+        require(out != nullptr, "band solver: null output");
+        require(ranks >= 1 && ranks <= kMaxBandRanks, "band solver: 1..8 ranks");
+        require(rank >= 0 && rank < ranks, "band solver: rank out of range");
+        require(width >= 1 && rows >= 1 && row0 >= 0 && row0 + rows <= full_height, "band solver: bad band rows");
+        require(rank > 0 || row0 == 0, "band solver: rank 0 owns the top row");
+        require(rank + 1 < ranks || row0 + rows == full_height, "band solver: the last rank owns the bottom row");
+        auto* s = new dco_band_solver;
+        s->ctx = ctx;
+        s->ranks = ranks;
+        s->rank = rank;
+        s->w = width;
+        s->row0 = row0;
+        s->rows = rows;
+        s->H = full_height;
+        s->n = static_cast<size_t>(width) * rows;
+        BandLayout L = band_layout(s->n);
+        s->arena_bytes = L.total;
+        cudaError_t e = cudaMalloc(&s->arena, L.total);
+        if (e != cudaSuccess) {
+            delete s;
+            fail(DCO_CUDA, std::string("band solver arena: ") + cudaGetErrorString(e));
+        }
+        cuda_check(cudaMemset(s->arena + L.words, 0, L.total - L.words), "band arena clear");
+        e = cudaMalloc(&s->desc_dev, kMaxBandRanks * sizeof(BandRank));
+        if (e != cudaSuccess) {
+            cudaFree(s->arena);
+            delete s;
+            fail(DCO_CUDA, std::string("band solver desc: ") + cudaGetErrorString(e));
+        }
+        *out = s;
+    });
+}
+
+void dco_band_solver_destroy(dco_band_solver* s) {
+    if (!s) return;
+    for (int r = 0; r < kMaxBandRanks; ++r)
+        if (s->ipc_opened[r]) cudaIpcCloseMemHandle(s->peer_base[r]);
+    cudaFree(s->desc_dev);
+    cudaFree(s->arena);
+    delete s;
+}
+
+int dco_band_solver_export(dco_band_solver* s, void* handle) {
+    if (!s) return DCO_INPUT;
+    return guarded(s->ctx, [&] {
+        require(handle != nullptr, "band solver: null handle buffer");
+        IpcBlob b;
+        memset(&b, 0, sizeof(b));
+        cuda_check(cudaIpcGetMemHandle(&b.handle, s->arena), "cudaIpcGetMemHandle");
+        b.rows = s->rows;
+        b.w = s->w;
+        b.rank = s->rank;
+        b.magic = 0x44434f42;
+        memset(handle, 0, DCO_BAND_HANDLE_BYTES);
+        memcpy(handle, &b, sizeof(b));
+    });
+}
+
+int dco_band_solver_connect(dco_band_solver* s, const void* handles) {
+    if (!s) return DCO_INPUT;
+    return guarded(s->ctx, [&] {
+        require(handles != nullptr, "band solver: null handles");
+        const char* h = static_cast<const char*>(handles);
+        for (int r = 0; r < s->ranks; ++r) {
+            IpcBlob b;
+            memcpy(&b, h + static_cast<size_t>(r) * DCO_BAND_HANDLE_BYTES, sizeof(b));
+            require(b.magic == 0x44434f42 && b.rank == r && b.w == s->w, "band solver: handle table is not rank-ordered");
+            s->peer_rows[r] = b.rows;
+            if (r == s->rank) {
+                s->peer_base[r] = s->arena;
+                continue;
+            }
+            void* p = nullptr;
+            cuda_check(cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            s->peer_base[r] = p;
+            s->ipc_opened[r] = true;
+        }
+        band_wire(s);
+    });
+}
+
+int dco_band_solver_connect_local(dco_band_solver* const* ss, int ranks) {
+    if (!ss || ranks < 1 || !ss[0]) return DCO_INPUT;
+    return guarded(ss[0]->ctx, [&] {
+        for (int k = 0; k < ranks; ++k) {
+            require(ss[k] && ss[k]->ranks == ranks && ss[k]->rank == k && ss[k]->w == ss[0]->w &&
+                        ss[k]->ctx == ss[0]->ctx,
+                    "band solver: local ranks must be rank-ordered on one context");
+            require(k == 0 || ss[k]->row0 == ss[k - 1]->row0 + ss[k - 1]->rows, "band solver: bands must tile the frame");
+        }
+        for (int k = 0; k < ranks; ++k) {
+            for (int r = 0; r < ranks; ++r) {
+                ss[k]->peer_base[r] = ss[r]->arena;
+                ss[k]->peer_rows[r] = ss[r]->rows;
+            }
+            band_wire(ss[k]);
+            ss[k]->local = true;
+        }
+    });
+}
+
+int dco_band_solve(dco_band_solver* s, const dco_system* sys, const dco_config* cfg, uint64_t anchors_total,
+                   double constant_total, float* dense, dco_solve_stats* stats) {
+    if (!s) return DCO_INPUT;
+    return guarded(s->ctx, [&] {
+        require(!s->local || s->ranks == 1, "band solver: connected locally; use dco_band_solve_local");
+        const int cap = (stats && stats->history) ? stats->history_cap : 0;
+        double* hist = cap > 0 ? static_cast<double*>(scratch(s->ctx, S_HIST, cap * sizeof(double))) : nullptr;
+        band_fill(s, sys, cfg, anchors_total, constant_total, dense, hist, cap);
+        dco_band_solver* one[1] = {s};
+        band_launch(s->ctx, one, 1);
+        band_stats(s->ctx, s, stats, hist);
+    });
+}
+
+int dco_band_solve_local(dco_band_solver* const* ss, int ranks, const dco_system* sys, const dco_config* cfg,
+                         uint64_t anchors_total, double constant_total, float* const* dense,
+                         dco_solve_stats* stats) {
+    if (!ss || ranks < 1 || !ss[0]) return DCO_INPUT;
+    return guarded(ss[0]->ctx, [&] {
+        dco_ctx* ctx = ss[0]->ctx;
+        const int cap = (stats && stats->history) ? stats->history_cap : 0;
+        double* hist = cap > 0 ? static_cast<double*>(scratch(ctx, S_HIST, cap * sizeof(double))) : nullptr;
+        for (int k = 0; k < ranks; ++k) {
+            require(ss[k]->ranks == ranks && ss[k]->ctx == ctx, "band solver: local ranks must share a context");
+            band_fill(ss[k], &sys[k], cfg, anchors_total, constant_total, dense[k], k == 0 ? hist : nullptr,
+                      k == 0 ? cap : 0);
+        }
+        band_launch(ctx, ss, ranks);
+        for (int k = 0; k < ranks; ++k) band_stats(ctx, ss[k], stats ? &stats[k] : nullptr, k == 0 ? hist : nullptr);
     });
 }
 

@@ -69,13 +69,14 @@ __device__ __forceinline__ int grid_reduce_index(int lane) {
 // sm: >= 32 * 16 doubles of shared scratch. partials: 2 * 16 * gridDim.x doubles.
 // kTailSync = false skips the closing CTA barrier: the caller guarantees a
 // __syncthreads() before sm is written again.
+// nb / bid: the participating blocks and this block's index among them (the
+// whole grid, or one rank's group of blocks in the row-band solver).
 template <int K, bool kTailSync = true>
-__device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, double* partials, unsigned& gen,
-                                               double* sm, double (&res)[K]) {
+__device__ __forceinline__ void barrier_reduce_of(double (&v)[K], GridBar* bar, double* partials, unsigned& gen,
+                                                  double* sm, double (&res)[K], int nb, int bid) {
     constexpr int P = ReducePad<K>::P;
     static_assert(K <= 16, "at most 16 values per reduction");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int nb = gridDim.x;
     double* table = partials + (gen & 1u) * (static_cast<size_t>(nb) * 16);
     // 1. warp level
     {
@@ -95,11 +96,11 @@ __device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, dou
         for (int w = g; w < nw; w += groups) s += sm[w * P + k];
 #pragma unroll
         for (int off = 16; off >= P; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane < K) __stcg(table + static_cast<size_t>(lane) * nb + blockIdx.x, s);
+        if (lane < K) __stcg(table + static_cast<size_t>(lane) * nb + bid, s);
         __syncwarp();
         // 3. arrive on this block's stripe; lanes 0..S-1 each wait for one stripe
         if (lane == 0)
-            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&bar->count[blockIdx.x % kGridBarStripes][0])
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&bar->count[bid % kGridBarStripes][0])
                          : "memory");
         if (lane < kGridBarStripes) {
             const unsigned members = static_cast<unsigned>((nb - lane + kGridBarStripes - 1) / kGridBarStripes);
@@ -128,6 +129,13 @@ __device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, dou
     for (int k = 0; k < K; ++k) res[k] = sres[k];
     ++gen;
     if (kTailSync) __syncthreads();  // sm reused by the next reduction
+}
+
+template <int K, bool kTailSync = true>
+__device__ __forceinline__ void barrier_reduce(double (&v)[K], GridBar* bar, double* partials, unsigned& gen,
+                                               double* sm, double (&res)[K]) {
+    barrier_reduce_of<K, kTailSync>(v, bar, partials, gen, sm, res, static_cast<int>(gridDim.x),
+                                    static_cast<int>(blockIdx.x));
 }
 
 }  // namespace dco_gpu

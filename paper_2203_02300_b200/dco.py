@@ -441,6 +441,99 @@ def solve_dense_depth(sys: ConstraintSystem, cfg: Config, history_cap=None):
     return dense, stats
 
 
+# ------------------------------------------------------- row-band solve ---
+def band_system(sys: ConstraintSystem, row0, rows):
+    """The dco_system of full rows [row0, row0 + rows) of a whole-frame system
+    (coup_v of the row above stays readable through the same allocation)."""
+    if not (0 <= row0 and rows >= 1 and row0 + rows <= sys.height):
+        raise InputError("band_system: rows outside the system")
+    s = native.System()
+    s.width, s.height = sys.width, rows
+    off = row0 * sys.width
+    s.diag = sys.diag.data_ptr() + 8 * off
+    s.coup_h = sys.coup_h.data_ptr() + 8 * off
+    s.coup_v = sys.coup_v.data_ptr() + 8 * off
+    s.rhs = sys.rhs.data_ptr() + 8 * off
+    s.initial = sys.initial.data_ptr() + 8 * off
+    s.anchored = sys.anchored.data_ptr() + off
+    s.constant_term = sys.constant_term
+    s.anchor_count = sys.anchor_count
+    return s
+
+
+def _stats_of(st, hist, cap):
+    return SolveStats(st.iterations, st.relative_residual, st.objective_initial, st.objective_final,
+                      list(hist[: min(cap, st.iterations + 1)]) if hist is not None else [])
+
+
+class BandSolver:
+    """One rank's share of a row-band densify solve (dco_band_solver)."""
+
+    def __init__(self, ranks, rank, width, row0, rows, full_height):
+        self.ranks, self.rank, self.width, self.row0, self.rows = ranks, rank, width, row0, rows
+        self.handle = ctypes.c_void_p()
+        _call(_lib().dco_band_solver_create, ranks, rank, width, row0, rows, full_height, ctypes.byref(self.handle))
+
+    def export(self):
+        buf = ctypes.create_string_buffer(native.BAND_HANDLE_BYTES)
+        native.check(context(), _lib().dco_band_solver_export(self.handle, buf))
+        return buf.raw
+
+    def connect(self, handles):
+        """handles: every rank's export(), rank order (CUDA IPC: one process per GPU)."""
+        blob = b"".join(handles)
+        if len(handles) != self.ranks or len(blob) != self.ranks * native.BAND_HANDLE_BYTES:
+            raise InputError("BandSolver.connect: one handle per rank")
+        native.check(context(), _lib().dco_band_solver_connect(self.handle, blob))
+
+    def solve(self, band_sys, cfg: Config, anchors_total, constant_total, history_cap=None):
+        dense = _f32((self.rows, self.width))
+        cap = cfg.solver_max_iter + 1 if history_cap is None else history_cap
+        hist = (ctypes.c_double * max(cap, 1))()
+        st = native.SolveStats()
+        st.history = ctypes.cast(hist, ctypes.POINTER(ctypes.c_double))
+        st.history_cap = cap
+        native.check(context(), _lib().dco_band_solve(self.handle, ctypes.byref(band_sys), ctypes.byref(cfg),
+                                                      anchors_total, constant_total, _p(dense), ctypes.byref(st)))
+        return dense, _stats_of(st, hist, cap)
+
+    def close(self):
+        if self.handle:
+            _lib().dco_band_solver_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def band_connect_local(solvers):
+    """All ranks in this process, on this GPU (the emulation of a multi-GPU
+    band solve with fewer GPUs than ranks)."""
+    arr = (ctypes.c_void_p * len(solvers))(*[s.handle.value for s in solvers])
+    native.check(context(), _lib().dco_band_solver_connect_local(arr, len(solvers)))
+
+
+def band_solve_local(solvers, band_systems, cfg: Config, anchors_total, constant_total, history_cap=None):
+    """One cooperative launch running every rank as a block group: (dense
+    per band, stats per band)."""
+    g = len(solvers)
+    dense = [_f32((s.rows, s.width)) for s in solvers]
+    cap = cfg.solver_max_iter + 1 if history_cap is None else history_cap
+    hist = (ctypes.c_double * max(cap, 1))()
+    sts = (native.SolveStats * g)()
+    sts[0].history = ctypes.cast(hist, ctypes.POINTER(ctypes.c_double))
+    sts[0].history_cap = cap
+    arr = (ctypes.c_void_p * g)(*[s.handle.value for s in solvers])
+    sys_arr = (native.System * g)(*band_systems)
+    out = (ctypes.c_void_p * g)(*[_p(d) for d in dense])
+    native.check(context(), _lib().dco_band_solve_local(arr, g, sys_arr, ctypes.byref(cfg), anchors_total,
+                                                        constant_total, out, sts))
+    return dense, [_stats_of(sts[k], hist if k == 0 else None, cap) for k in range(g)]
+
+
 # ------------------------------------------------------------- composite ---
 def composite(real_rgb, dense, virt_rgb, virt_depth):
     """composite, occlude.cpp:171-194: (color, mask)."""

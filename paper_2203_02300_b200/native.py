@@ -8,6 +8,7 @@ import os
 
 from .config import Config, raise_for
 
+BAND_HANDLE_BYTES = 128  # DCO_BAND_HANDLE_BYTES
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdco_gpu.so")
 
@@ -140,6 +141,17 @@ SIGNATURES = {
     "dco_band_plan": (c_int, [CFG, c_int, c_int, c_int, c_int, ctypes.POINTER(Band)]),
     "dco_band_carry_bytes": (c_size_t, [CFG, c_int]),
     "dco_stereo_band": (c_int, [c_void_p, P, P, ctypes.POINTER(Band), CFG, c_int, c_int, P, P, P, P]),
+    "dco_band_solver_create": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p)]),
+    "dco_band_solver_destroy": (None, [c_void_p]),
+    "dco_band_solver_export": (c_int, [c_void_p, c_void_p]),
+    "dco_band_solver_connect": (c_int, [c_void_p, c_void_p]),
+    "dco_band_solver_connect_local": (c_int, [ctypes.POINTER(c_void_p), c_int]),
+    "dco_band_solve": (c_int, [c_void_p, ctypes.POINTER(System), CFG, c_uint64, c_double, P, ctypes.POINTER(SolveStats)]),
+    "dco_band_solve_local": (
+        c_int,
+        [ctypes.POINTER(c_void_p), c_int, ctypes.POINTER(System), CFG, c_uint64, c_double, ctypes.POINTER(c_void_p),
+         ctypes.POINTER(SolveStats)],
+    ),
     "dco_stream_create": (c_int, [c_void_p, c_int, c_int, CFG, ctypes.POINTER(c_void_p)]),
     "dco_stream_destroy": (None, [c_void_p]),
     "dco_stream_set_virtual": (c_int, [c_void_p, P, P]),
