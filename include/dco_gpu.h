@@ -353,6 +353,24 @@ int dco_stereo_band(dco_ctx* ctx, const float* left_sub, const float* right_sub,
  * band's first row, coup_v readable one row above it when row0 > 0. The
  * Krylov scalars are the same on every rank; the result matches
  * dco_solve_dense_depth within the solver tolerance (densify.cpp:141-222). */
+/* Row-band assembly (densify.cpp:37-116). The frame-wide sparse mean
+ * (densify.cpp:60-68) is the one global input: every band reports
+ * {sum, sum of |v|, count, min ulp exponent} of its owned rows (host doubles),
+ * the ranks exchange them, and dco_band_sparse_mean combines them in rank
+ * order -- exact (the sequential sum's bits) whenever the guard holds
+ * (*exact = 1); otherwise the caller gathers the full sparse map and uses
+ * dco_sparse_mean. dco_band_assemble fills the system of the sub-frame rows it
+ * is given (inputs offset to the sub-frame's first row, an even full row;
+ * m_fuse offset by half of it) with the frame's mean, and returns anchors and
+ * constant term of the owned sub-frame rows [own0, own0 + own_rows). */
+int dco_band_sparse_stats(dco_ctx* ctx, const float* sparse_rows, size_t n, double* out4);
+int dco_band_sparse_mean(const double* stats, int bands, double* mean, int* exact);
+int dco_sparse_mean(dco_ctx* ctx, const float* sparse, size_t n, double* mean);
+int dco_band_assemble(dco_ctx* ctx, const float* sparse, const uint8_t* edges, const float* m_fuse, int qw, int qh,
+                      const float* m_i, const float* d_pre, int w, int h, int own0, int own_rows,
+                      const dco_config* cfg, double sparse_mean, dco_system* sys, uint64_t* anchors,
+                      double* constant);
+
 #define DCO_BAND_HANDLE_BYTES 128
 typedef struct dco_band_solver dco_band_solver;
 int dco_band_solver_create(dco_ctx* ctx, int ranks, int rank, int width, int row0, int rows, int full_height,

@@ -252,6 +252,21 @@ __global__ void k_anchor_const(const uint8_t* __restrict__ anch, const float* __
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// (sum, |sum|) of k_sparse_stats' block partials
+__global__ void k_sparse_pair_sums(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+    __shared__ double sm[32 * 2];
+    double v[2] = {0.0, 0.0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+        v[0] += part[2 * b];
+        v[1] += part[2 * b + 1];
+    }
+    block_sum<2>(v, sm);
+    if (threadIdx.x == 0) {
+        out[0] = v[0];
+        out[1] = v[1];
+    }
+}
+
 __global__ void k_reduce_parts(const double* __restrict__ part, int nparts, double* __restrict__ out) {
     __shared__ double sm[32];
     double v[1] = {0.0};
@@ -1048,6 +1063,143 @@ int dco_assemble_system(dco_ctx* ctx, const float* sparse, const uint8_t* edges,
         cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
         sys->constant_term = hp[0];
         sys->anchor_count = reinterpret_cast<unsigned long long*>(hp)[1];
+    });
+}
+
+// ---------------------------------------------------- row-band assembly ---
+int dco_band_sparse_stats(dco_ctx* ctx, const float* sparse, size_t n, double* out) {
+    return guarded(ctx, [&] {
+        require(out != nullptr, "band_sparse_stats: null output");
+        const int nblk = 296;
+        char* scr = static_cast<char*>(scratch(ctx, S_STATS, 4096 + nblk * 2 * sizeof(double) * 2));
+        unsigned long long* count = reinterpret_cast<unsigned long long*>(scr);
+        int* min_exp = reinterpret_cast<int*>(scr + 8);
+        double* sums = reinterpret_cast<double*>(scr + 16);
+        double* part = reinterpret_cast<double*>(scr + 4096);
+        cuda_check(cudaMemsetAsync(scr, 0, 16, ctx->stream), "memset");
+        cuda_check(cudaMemsetAsync(min_exp, 0x3f, sizeof(int), ctx->stream), "memset");
+        k_sparse_stats<<<nblk, 256, 0, ctx->stream>>>(sparse, n, part, count, min_exp);
+        launched(ctx, "k_sparse_stats");
+        // band totals: a fixed tree over the block partials (exact under the guard)
+        k_sparse_pair_sums<<<1, 256, 0, ctx->stream>>>(part, nblk, sums);
+        launched(ctx, "k_sparse_pair_sums");
+        char* hp = static_cast<char*>(pinned_host(ctx, 64));
+        cuda_check(cudaMemcpyAsync(hp, scr, 32, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        const unsigned long long c = *reinterpret_cast<unsigned long long*>(hp);
+        const int me = *reinterpret_cast<int*>(hp + 8);
+        out[0] = reinterpret_cast<double*>(hp + 16)[0];
+        out[1] = reinterpret_cast<double*>(hp + 16)[1];
+        out[2] = static_cast<double>(c);
+        out[3] = static_cast<double>(me);
+    });
+}
+
+int dco_band_sparse_mean(const double* stats, int bands, double* mean, int* exact) {
+    if (!stats || !mean || !exact || bands < 1) return DCO_INPUT;
+    double sum = 0.0, abs_sum = 0.0, count = 0.0, me = 1e300;
+    for (int k = 0; k < bands; ++k) {
+        sum += stats[4 * k];
+        abs_sum += stats[4 * k + 1];
+        count += stats[4 * k + 2];
+        if (stats[4 * k + 2] > 0.0) me = std::min(me, stats[4 * k + 3]);
+    }
+    *exact = 1;
+    if (count == 0.0) {
+        *mean = 0.0;
+        return DCO_OK;
+    }
+    // the guard of k_sparse_mean, frame-wide: every partial sum of the valid
+    // values is a multiple of 2^min_exp below 2^(53 + min_exp), so every band's
+    // sum and their sum here are exact -- the sequential sum's bits
+    if (!(abs_sum * (1.0 + 1e-9) < ldexp(1.0, 53 + static_cast<int>(me)))) {
+        *exact = 0;
+        return DCO_OK;
+    }
+    *mean = sum / count;
+    return DCO_OK;
+}
+
+int dco_sparse_mean(dco_ctx* ctx, const float* sparse, size_t n, double* mean) {
+    return guarded(ctx, [&] {
+        const int nblk = 296;
+        char* scr = static_cast<char*>(scratch(ctx, S_STATS, 4096 + nblk * 2 * sizeof(double) * 2));
+        unsigned long long* count = reinterpret_cast<unsigned long long*>(scr);
+        int* min_exp = reinterpret_cast<int*>(scr + 8);
+        double* m = reinterpret_cast<double*>(scr + 16);
+        double* part = reinterpret_cast<double*>(scr + 4096);
+        cuda_check(cudaMemsetAsync(scr, 0, 16, ctx->stream), "memset");
+        cuda_check(cudaMemsetAsync(min_exp, 0x3f, sizeof(int), ctx->stream), "memset");
+        k_sparse_stats<<<nblk, 256, 0, ctx->stream>>>(sparse, n, part, count, min_exp);
+        launched(ctx, "k_sparse_stats");
+        k_sparse_mean<<<1, 256, 0, ctx->stream>>>(sparse, n, part, nblk, count, min_exp, m);
+        launched(ctx, "k_sparse_mean");
+        double* hp = static_cast<double*>(pinned_host(ctx, 64));
+        cuda_check(cudaMemcpyAsync(hp, m, 8, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        *mean = hp[0];
+    });
+}
+
+int dco_band_assemble(dco_ctx* ctx, const float* sparse, const uint8_t* edges, const float* mf, int qw, int qh,
+                      const float* mi, const float* pre, int w, int h, int own0, int own_rows,
+                      const dco_config* cfg, double sparse_mean, dco_system* sys, uint64_t* anchors,
+                      double* constant) {
+    return guarded(ctx, [&] {
+        require(sys && sys->diag && sys->coup_h && sys->coup_v && sys->rhs && sys->initial && sys->anchored,
+                "band_assemble: system buffers missing");
+        require(anchors && constant, "band_assemble: null outputs");
+        require(qw >= 1 && qh >= 1 && w >= 1 && h >= 1, "band_assemble: empty inputs");
+        require(own0 >= 0 && own_rows >= 1 && own0 + own_rows <= h, "band_assemble: owned rows outside the sub-frame");
+        if (cfg->lambda_s2 <= 0.0) pre = nullptr;  // densify.cpp:48
+        sys->width = w;
+        sys->height = h;
+        char* scr = static_cast<char*>(scratch(ctx, S_FLAG_ASM, 64));
+        double* mean_dev = reinterpret_cast<double*>(scr + 16);
+        cuda_check(cudaMemcpyAsync(mean_dev, &sparse_mean, 8, cudaMemcpyHostToDevice, ctx->stream), "mean");
+        AsmArgs a;
+        a.w = w;
+        a.h = h;
+        a.qw = qw;
+        a.qh = qh;
+        a.lambda_d = cfg->lambda_d;
+        a.lambda_s = cfg->lambda_s;
+        a.lambda_s2 = cfg->lambda_s2;
+        a.sparse = sparse;
+        a.edges = edges;
+        a.mf = mf;
+        a.mi = mi;
+        a.pre = pre;
+        a.pre_valid = nullptr;
+        a.diag = sys->diag;
+        a.ch = sys->coup_h;
+        a.cv = sys->coup_v;
+        a.rhs = sys->rhs;
+        a.init = sys->initial;
+        a.anchored = sys->anchored;
+        a.sparse_mean = mean_dev;
+        dim3 b(32, 8);
+        k_assemble<<<grid2(w, h, b), b, 0, ctx->stream>>>(a);
+        launched(ctx, "k_assemble");
+        // anchors and constant term of the owned rows only
+        const size_t off = static_cast<size_t>(own0) * w, n = static_cast<size_t>(own_rows) * w;
+        const int nblk = 296;
+        double* part = static_cast<double*>(scratch(ctx, S_STATS, 4096 + nblk * 2 * sizeof(double) * 2));
+        unsigned long long* adev = reinterpret_cast<unsigned long long*>(scr + 8);
+        double* cdev = reinterpret_cast<double*>(scr);
+        cuda_check(cudaMemsetAsync(adev, 0, 8, ctx->stream), "memset");
+        k_anchor_const<<<nblk, 256, 0, ctx->stream>>>(sys->anchored + off, sparse + off, pre ? pre + off : nullptr,
+                                                      nullptr, n, cfg->lambda_d, cfg->lambda_s2, adev, part);
+        launched(ctx, "k_anchor_const");
+        k_reduce_parts<<<1, 256, 0, ctx->stream>>>(part, nblk, cdev);
+        launched(ctx, "k_reduce_parts");
+        double* hp = static_cast<double*>(pinned_host(ctx, 64));
+        cuda_check(cudaMemcpyAsync(hp, scr, 16, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+        *constant = hp[0];
+        *anchors = reinterpret_cast<unsigned long long*>(hp)[1];
+        sys->constant_term = *constant;
+        sys->anchor_count = *anchors;
     });
 }
 

@@ -141,6 +141,14 @@ SIGNATURES = {
     "dco_band_plan": (c_int, [CFG, c_int, c_int, c_int, c_int, ctypes.POINTER(Band)]),
     "dco_band_carry_bytes": (c_size_t, [CFG, c_int]),
     "dco_stereo_band": (c_int, [c_void_p, P, P, ctypes.POINTER(Band), CFG, c_int, c_int, P, P, P, P]),
+    "dco_band_sparse_stats": (c_int, [c_void_p, P, c_size_t, ctypes.POINTER(c_double)]),
+    "dco_band_sparse_mean": (c_int, [ctypes.POINTER(c_double), c_int, ctypes.POINTER(c_double), ctypes.POINTER(c_int)]),
+    "dco_sparse_mean": (c_int, [c_void_p, P, c_size_t, ctypes.POINTER(c_double)]),
+    "dco_band_assemble": (
+        c_int,
+        [c_void_p, P, P, P, c_int, c_int, P, P, c_int, c_int, c_int, c_int, CFG, c_double, ctypes.POINTER(System),
+         ctypes.POINTER(c_uint64), ctypes.POINTER(c_double)],
+    ),
     "dco_band_solver_create": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p)]),
     "dco_band_solver_destroy": (None, [c_void_p]),
     "dco_band_solver_export": (c_int, [c_void_p, c_void_p]),

@@ -1,0 +1,222 @@
+"""Row-band frames: one frame split over G ranks (BASELINE config D,
+3840x2160 D=256 "row-band partitioning with halo exchange over NVLink").
+
+Per composited frame (pipeline.cpp:183-258), band k of G:
+  * stereo on its quarter rows plus the recompute halo (dco_stereo_band); the
+    aggregation column prefix arrives from band k-1 and leaves for band k+1
+    (the chain is the one true data exchange of the stereo stage);
+  * flow, amplitude fusion, box filter, normalisation, blur and contours run
+    on the whole frame on every rank (they are 5 % of a 4K frame, and the
+    global maxima of contour.cpp:139-141/197-200 and the hysteresis flood then
+    need no exchange);
+  * the frame-wide sparse mean is combined from every band's exact partial
+    sums (dco_band_sparse_mean), then each band assembles its full rows plus a
+    2-row halo (dco_band_assemble);
+  * the PCG + MR solve runs over all bands at once (dco_band_solver: reduction
+    and p halo through peer memory inside one persistent kernel per GPU);
+  * each band composites its own rows.
+
+Links: LocalLinks runs all G bands in this process on one GPU (the solve as
+one cooperative launch over all bands); DistLinks gives each rank one band and
+moves the carries, the sparse statistics and the solver handles with
+torch.distributed (NCCL on GPUs). The band code is the same for both.
+"""
+import math
+
+import torch
+
+from . import dco
+from .config import Config, UnsolvableFrameError
+
+
+class LocalLinks:
+    """Every band in this process (fewer GPUs than bands)."""
+
+    def __init__(self, bands):
+        self.bands = bands
+        self.owned = list(range(bands))
+        self._carry = {}
+
+    def put_carry(self, k, t):
+        self._carry[k + 1] = t
+
+    def get_carry(self, k, like):
+        return self._carry.pop(k)
+
+    def gather_stats(self, stats):
+        return [stats[k] for k in range(self.bands)]
+
+    def gather_bytes(self, blobs):
+        return [blobs[k] for k in range(self.bands)]
+
+
+class DistLinks:
+    """One band per rank over torch.distributed (rank k owns band k)."""
+
+    def __init__(self, group_dist, world, rank, device=None):
+        self.dist = group_dist
+        self.bands = world
+        self.rank = rank
+        self.owned = [rank]
+        self.device = device
+
+    def put_carry(self, k, t):
+        self.dist.send(t, dst=k + 1)
+
+    def get_carry(self, k, like):
+        t = torch.empty_like(like)
+        self.dist.recv(t, src=k - 1)
+        return t
+
+    def gather_stats(self, stats):
+        mine = torch.tensor(stats[self.rank], dtype=torch.float64, device=self.device)
+        out = [torch.empty_like(mine) for _ in range(self.bands)]
+        self.dist.all_gather(out, mine)
+        return [o.tolist() for o in out]
+
+    def gather_bytes(self, blobs):
+        out = [None] * self.bands
+        self.dist.all_gather_object(out, blobs[self.rank])
+        return out
+
+
+class RowBandFrames:
+    """The row-band frame loop of one stream: owns the band plans, the band
+    solvers and the previous dense rows (the d_pre chain, pipeline.cpp:133,235)."""
+
+    def __init__(self, full_w, full_h, cfg: Config, links):
+        self.fw, self.fh, self.cfg, self.links = full_w, full_h, cfg, links
+        g = links.bands
+        self.plans = {k: dco.band_plan(cfg, full_w, full_h, g, k) for k in links.owned}
+        self.solvers = {}
+        for k, b in self.plans.items():
+            self.solvers[k] = dco.BandSolver(g, k, full_w, b.frow0, b.frow1 - b.frow0, full_h)
+        if isinstance(links, LocalLinks):
+            dco.band_connect_local([self.solvers[k] for k in range(g)])
+        else:
+            handles = links.gather_bytes({k: s.export() for k, s in self.solvers.items()})
+            for s in self.solvers.values():
+                s.connect(handles)
+        self.prev = {}  # band -> dense rows of the previous frame
+        self.iterations = 0
+
+    def close(self):
+        for s in self.solvers.values():
+            s.close()
+        self.solvers = {}
+
+    def _sub(self, b):
+        """Full rows of a band's assembly sub-frame: owned + 2 (even start)."""
+        return max(0, b.frow0 - 2), min(self.fh, b.frow1 + 2)
+
+    def frame(self, past_q, mid_q, future_q, mid_gray, right_q, mid_rgb, vrgb=None, vdepth=None):
+        """One composited frame. Inputs are whole-frame device tensors (quarter
+        lefts of the keyframe window, the middle frame's gray, right quarter and
+        RGB; optional virtual layer). Returns {band: dict(dense, composite,
+        mask, sparse, rows)} for the bands this process owns."""
+        cfg, fw, fh, L = self.cfg, self.fw, self.fh, self.links
+        # whole-frame contour inputs on every rank (contour.cpp, no exchange)
+        fp = dco.compute_flow(mid_q, past_q, cfg)
+        ff = dco.compute_flow(mid_q, future_q, cfg)
+        mp = dco.gradient_amplitude(dco.flow_to_polar(*fp, with_theta=False)[0])
+        mf = dco.gradient_amplitude(dco.flow_to_polar(*ff, with_theta=False)[0])
+        m_fuse = dco.normalize_amplitude(dco.box_filter(dco.fuse_amplitudes(fp, ff, mp, mf, cfg), cfg.box_radius))
+        edges, m_i = dco.extract_depth_contours_prefiltered(dco.gaussian_blur(mid_gray, cfg.gauss_sigma), m_fuse, cfg)
+        qw = m_fuse.shape[1]
+        # stereo per band, carries down the chain
+        sparse = {}
+        for k in sorted(self.plans):
+            b = self.plans[k]
+            carry = None
+            if b.carry_row > 0:
+                carry = L.get_carry(k, torch.empty(dco.band_carry_elems(cfg, fw), dtype=torch.float64, device="cuda"))
+            _, sparse[k], carry_out = dco.stereo_band(mid_q[b.sub0:b.sub1].contiguous(),
+                                                      right_q[b.sub0:b.sub1].contiguous(), b, cfg, fw, fh, carry)
+            if carry_out is not None:
+                L.put_carry(k, carry_out)
+        # frame-wide sparse mean from the bands' exact partials
+        stats = {k: self._sparse_stats(sparse[k]) for k in self.plans}
+        allstats = L.gather_stats(stats)
+        mean, exact = self._combine(allstats)
+        if not exact:
+            raise NotImplementedError("row bands: sparse mean outside the exact guard (gather the full map)")
+        self._mean = mean
+        # assembly of each band's rows (+ 2-row halo)
+        systems, anchors, const = {}, {}, {}
+        for k, b in self.plans.items():
+            s0, s1 = self._sub(b)
+            sub_sparse = torch.full((s1 - s0, fw), math.nan, dtype=torch.float32, device="cuda")
+            sub_sparse[b.frow0 - s0:b.frow1 - s0] = sparse[k]
+            pre = None
+            if k in self.prev and cfg.lambda_s2 > 0.0:
+                pre = torch.full((s1 - s0, fw), math.nan, dtype=torch.float32, device="cuda")
+                pre[b.frow0 - s0:b.frow1 - s0] = self.prev[k]
+            sys = dco.ConstraintSystem(fw, s1 - s0)
+            anchors[k], const[k] = self._assemble(sub_sparse, edges[s0:s1], m_fuse[s0 // 2:], qw,
+                                                  m_i[s0:s1], pre, b.frow0 - s0, b.frow1 - b.frow0, sys)
+            systems[k] = (sys, b.frow0 - s0)
+        tot = L.gather_stats({k: [float(anchors[k]), const[k], 0.0, 0.0] for k in self.plans})
+        anchors_total = int(sum(t[0] for t in tot))
+        const_total = sum(t[1] for t in tot)
+        # the solve over all bands
+        dense = {}
+        if anchors_total == 0:  # pipeline.cpp:236-242: keep the previous dense map
+            for k, b in self.plans.items():
+                dense[k] = self.prev.get(k, torch.full((b.frow1 - b.frow0, fw), math.nan, device="cuda"))
+            unsolvable = True
+        else:
+            views = {k: dco.band_system(sys, r0, self.plans[k].frow1 - self.plans[k].frow0)
+                     for k, (sys, r0) in systems.items()}
+            if isinstance(L, LocalLinks):
+                ks = sorted(self.plans)
+                out, st = dco.band_solve_local([self.solvers[k] for k in ks], [views[k] for k in ks], cfg,
+                                               anchors_total, const_total, history_cap=0)
+                dense = dict(zip(ks, out))
+                self.iterations = st[0].iterations
+            else:
+                for k in self.plans:
+                    dense[k], st = self.solvers[k].solve(views[k], cfg, anchors_total, const_total, history_cap=0)
+                    self.iterations = st.iterations
+            unsolvable = False
+        # composite of each band's rows
+        res = {}
+        for k, b in self.plans.items():
+            r0, r1 = b.frow0, b.frow1
+            vr = vrgb[r0:r1] if vrgb is not None else torch.zeros((r1 - r0, fw, 3), device="cuda")
+            vd = vdepth[r0:r1] if vdepth is not None else torch.full((r1 - r0, fw), math.nan, device="cuda")
+            comp, mask = dco.composite(mid_rgb[r0:r1].contiguous(), dense[k], vr.contiguous(), vd.contiguous())
+            res[k] = dict(dense=dense[k], composite=comp, mask=mask, sparse=sparse[k], rows=(r0, r1),
+                          unsolvable=unsolvable)
+            self.prev[k] = dense[k]
+        return res
+
+    @staticmethod
+    def _sparse_stats(rows):
+        import ctypes
+
+        out = (ctypes.c_double * 4)()
+        dco._call(dco._lib().dco_band_sparse_stats, dco._p(rows), rows.numel(), out)
+        return list(out)
+
+    @staticmethod
+    def _combine(allstats):
+        import ctypes
+
+        flat = (ctypes.c_double * (4 * len(allstats)))(*[v for s in allstats for v in s])
+        mean, exact = ctypes.c_double(), ctypes.c_int()
+        st = dco._lib().dco_band_sparse_mean(flat, len(allstats), ctypes.byref(mean), ctypes.byref(exact))
+        if st != 0:
+            raise UnsolvableFrameError("dco_band_sparse_mean failed")
+        return mean.value, bool(exact.value)
+
+    def _assemble(self, sparse, edges, m_fuse, qw, m_i, pre, own0, own_rows, sys):
+        import ctypes
+
+        w, h = self.fw, sparse.shape[0]
+        qh = m_fuse.shape[0]
+        cs = sys.c_struct()
+        anchors, const = ctypes.c_uint64(), ctypes.c_double()
+        dco._call(dco._lib().dco_band_assemble, dco._p(sparse), dco._p(edges.contiguous()), dco._p(m_fuse.contiguous()),
+                  qw, qh, dco._p(m_i.contiguous()), dco._p(pre), w, h, own0, own_rows, ctypes.byref(self.cfg),
+                  self._mean, ctypes.byref(cs), ctypes.byref(anchors), ctypes.byref(const))
+        return anchors.value, const.value

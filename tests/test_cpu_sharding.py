@@ -59,3 +59,43 @@ def test_stream_seed_bounds():
     assert stream_seeds(0, 2) == [61, 62] and stream_seeds(1, 2) == [158, 159]
     with pytest.raises(ValueError):
         stream_seeds(0, 97)
+
+
+def _band_links_worker(rank, world, port, out):
+    """DistLinks (rowband.py) over gloo: the carry chain, the stats gather and
+    the solver-handle gather, as the row-band frame uses them under NCCL."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    from paper_2203_02300_b200.rowband import DistLinks
+
+    g = Group(world, rank, "gloo")
+    links = DistLinks(torch.distributed, world, rank, device="cpu")
+    like = torch.empty(6, dtype=torch.float64)
+    got = None
+    if rank > 0:
+        got = links.get_carry(rank, like).tolist()
+    if rank + 1 < world:
+        links.put_carry(rank, torch.arange(6, dtype=torch.float64) + 10.0 * rank)
+    stats = links.gather_stats({rank: [1.0 + rank, 2.0 * rank, 3.0, -24.0 - rank]})
+    blobs = links.gather_bytes({rank: bytes([rank]) * 128})
+    g.close()
+    out.put((rank, got, stats, blobs))
+
+
+def test_band_links_two_and_three_ranks():
+    for world in (2, 3):
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _free_port()
+        ps = [ctx.Process(target=_band_links_worker, args=(r, world, port, q)) for r in range(world)]
+        for p in ps:
+            p.start()
+        res = sorted(q.get(timeout=120) for _ in range(world))
+        for p in ps:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        for rank, got, stats, blobs in res:
+            # band k receives exactly band k-1's carry
+            assert got == (None if rank == 0 else [10.0 * (rank - 1) + i for i in range(6)])
+            # every rank holds every band's statistics, rank-ordered
+            assert stats == [[1.0 + r, 2.0 * r, 3.0, -24.0 - r] for r in range(world)]
+            assert blobs == [bytes([r]) * 128 for r in range(world)]
