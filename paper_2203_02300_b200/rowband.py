@@ -99,6 +99,23 @@ class RowBandFrames:
                 s.connect(handles)
         self.prev = {}  # band -> dense rows of the previous frame
         self.iterations = 0
+        self.timing = False  # CUDA-event spans per phase into self.spans (ms, summed)
+        self.spans = {}
+        self._marks = []
+
+    def _mark(self, name):
+        if self.timing:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self._marks.append((name, e))
+
+    def _close_marks(self):
+        if not self.timing or not self._marks:
+            return
+        torch.cuda.synchronize()
+        for (_, a), (name, b) in zip(self._marks, self._marks[1:]):
+            self.spans[name] = self.spans.get(name, 0.0) + a.elapsed_time(b)
+        self._marks = []
 
     def close(self):
         for s in self.solvers.values():
@@ -115,6 +132,7 @@ class RowBandFrames:
         RGB; optional virtual layer). Returns {band: dict(dense, composite,
         mask, sparse, rows)} for the bands this process owns."""
         cfg, fw, fh, L = self.cfg, self.fw, self.fh, self.links
+        self._mark("start")
         # whole-frame contour inputs on every rank (contour.cpp, no exchange)
         fp = dco.compute_flow(mid_q, past_q, cfg)
         ff = dco.compute_flow(mid_q, future_q, cfg)
@@ -123,6 +141,7 @@ class RowBandFrames:
         m_fuse = dco.normalize_amplitude(dco.box_filter(dco.fuse_amplitudes(fp, ff, mp, mf, cfg), cfg.box_radius))
         edges, m_i = dco.extract_depth_contours_prefiltered(dco.gaussian_blur(mid_gray, cfg.gauss_sigma), m_fuse, cfg)
         qw = m_fuse.shape[1]
+        self._mark("flow+contour")
         # stereo per band, carries down the chain
         sparse = {}
         for k in sorted(self.plans):
@@ -134,6 +153,7 @@ class RowBandFrames:
                                                       right_q[b.sub0:b.sub1].contiguous(), b, cfg, fw, fh, carry)
             if carry_out is not None:
                 L.put_carry(k, carry_out)
+        self._mark("stereo")
         # frame-wide sparse mean from the bands' exact partials
         stats = {k: self._sparse_stats(sparse[k]) for k in self.plans}
         allstats = L.gather_stats(stats)
@@ -158,6 +178,7 @@ class RowBandFrames:
         tot = L.gather_stats({k: [float(anchors[k]), const[k], 0.0, 0.0] for k in self.plans})
         anchors_total = int(sum(t[0] for t in tot))
         const_total = sum(t[1] for t in tot)
+        self._mark("assemble")
         # the solve over all bands
         dense = {}
         if anchors_total == 0:  # pipeline.cpp:236-242: keep the previous dense map
@@ -178,6 +199,7 @@ class RowBandFrames:
                     dense[k], st = self.solvers[k].solve(views[k], cfg, anchors_total, const_total, history_cap=0)
                     self.iterations = st.iterations
             unsolvable = False
+        self._mark("solve")
         # composite of each band's rows
         res = {}
         for k, b in self.plans.items():
@@ -188,6 +210,8 @@ class RowBandFrames:
             res[k] = dict(dense=dense[k], composite=comp, mask=mask, sparse=sparse[k], rows=(r0, r1),
                           unsolvable=unsolvable)
             self.prev[k] = dense[k]
+        self._mark("composite")
+        self._close_marks()
         return res
 
     @staticmethod
