@@ -22,7 +22,7 @@ namespace dco_gpu {
 namespace {
 
 constexpr int kMaxBandRanks = 8;
-constexpr int kBandThreads = 512;
+constexpr int kBandThreads = 384;
 constexpr int kBandB = 2;
 
 // Per-rank arena layout (doubles): p[2], r[2], q[2], prec, x, xs, rs (n each),
