@@ -321,7 +321,7 @@ int dco_stream_load_state(dco_stream* s, const void* host_buf, size_t len);
  * rows each side (I = hist_iterations, Rc = census half-height), so every
  * owned row is bit-equal to the whole frame's. The one true exchange is the
  * aggregation's sequential column prefix (stereo.cpp:203-215): band k starts
- * it at carry_row from band k-1's exact prefix (qw * nd doubles, [x][d]) and
+ * it at carry_row from band k-1's exact prefix (nd * qw doubles, [d][x]) and
  * exports its prefix at carry_out_row to band k+1 -- a chain over bands. No
  * reference function is replaced; this is the multi-GPU split of
  * dco_stereo_sparse_depth (pipeline.cpp:184-195). */
@@ -334,7 +334,7 @@ typedef struct dco_band {
     int halo;             /* recompute halo in quarter rows                        */
 } dco_band;
 int dco_band_plan(const dco_config* cfg, int full_w, int full_h, int bands, int index, dco_band* out);
-/* Bytes of one carry buffer: (full_w / 2) * (d_max - d_min + 1) doubles. */
+/* Bytes of one carry buffer: (d_max - d_min + 1) * (full_w / 2) doubles, [d][x]. */
 size_t dco_band_carry_bytes(const dco_config* cfg, int full_w);
 /* Stereo chain of one band. left_sub / right_sub: quarter rows [sub0, sub1)
  * (qw = full_w / 2 wide). carry_in: required when carry_row > 0; carry_out:
@@ -343,6 +343,18 @@ size_t dco_band_carry_bytes(const dco_config* cfg, int full_w);
 int dco_stereo_band(dco_ctx* ctx, const float* left_sub, const float* right_sub, const dco_band* band,
                     const dco_config* cfg, int full_w, int full_h, const double* carry_in, double* carry_out,
                     float* disparity, float* sparse);
+/* The same in three phases, so that under a multi-GPU chain only the vertical
+ * pass waits for the carry, and the carry can travel in disparity chunks:
+ * begin (cross windows, cost, horizontal pass), vpass over slices [d0, d1)
+ * (d0 a multiple of 32; carry buffers of (d1-d0) * qw doubles, [d][x]), end
+ * (WTA, refinement, sparse). State lives in the context between the calls:
+ * no other stereo call on ctx until end. */
+int dco_stereo_band_begin(dco_ctx* ctx, const float* left_sub, const float* right_sub, const dco_band* band,
+                          const dco_config* cfg, int full_w, int full_h);
+int dco_stereo_band_vpass(dco_ctx* ctx, const dco_band* band, const dco_config* cfg, int full_w, int full_h, int d0,
+                          int d1, const double* carry_in, double* carry_out);
+int dco_stereo_band_end(dco_ctx* ctx, const dco_band* band, const dco_config* cfg, int full_w, int full_h,
+                        float* disparity, float* sparse);
 
 /* Row-band densify (SURVEY 8e "1-row p halo per SpMV plus an all-reduce of
  * the scalar groups per iteration"): the PCG + MR solve of one frame's system

@@ -540,32 +540,32 @@ __global__ void __launch_bounds__(kAggThreads) k_agg_h2(const float* __restrict_
 // Pipelined vertical pass: same chain, rounding and division as k_agg_vpass.
 // Block = 32 slices x 4 columns.
 // kBand (row bands, DESIGN 7): the column prefix starts at row c0 from the
-// exact prefix of the rows above the band (carry_in, [x][d] doubles, or 0)
-// -- rows < c0 add nothing -- and the prefix before row e is exported to
+// exact prefix of the rows above the band (carry_in, [d - k0][x] doubles, or
+// 0) -- rows < c0 add nothing -- and the prefix before row e is exported to
 // carry_out for the next band. Same chain, so the exact rows are bit-equal to
-// the whole frame's.
+// the whole frame's. Slices [k0, k1) only (a chunk of the carry chain).
 template <int kPF, bool kBand = false>
 __global__ void __launch_bounds__(kAggThreads) k_agg_v2(const double* __restrict__ hsum, int w, int h, int nd,
                                                         const uint32_t* __restrict__ vinfo, int lag, int ring_n,
                                                         float* __restrict__ out, const double* __restrict__ carry_in = nullptr,
                                                         int c0 = 0, double* __restrict__ carry_out = nullptr,
-                                                        int e = -1) {
+                                                        int e = -1, int k0 = 0, int k1 = 0) {
     extern __shared__ double ring[];
     const int lane = threadIdx.x, tid = threadIdx.y * 32 + threadIdx.x;
-    const int k = blockIdx.x * 32 + lane;
+    const int k = (kBand ? k0 : 0) + blockIdx.x * 32 + lane;
     const int x = blockIdx.y * 4 + threadIdx.y;
-    if (x >= w || k >= nd) return;
+    if (x >= w || k >= (kBand ? k1 : nd)) return;
     const size_t row = static_cast<size_t>(w) * nd;
     const double* lp = hsum + static_cast<size_t>(x) * nd + k;
     float* dst = out + static_cast<size_t>(x) * nd + k;
     const uint32_t* info = vinfo + x;
     double* rg = ring + tid;
     double C = 0.0;
-    if (kBand && carry_in) C = carry_in[static_cast<size_t>(x) * nd + k];
+    if (kBand && carry_in) C = carry_in[static_cast<size_t>(k - k0) * w + x];
     rg[0] = C;
     int s1 = 0;
     auto note = [&](int y) {  // C is now the prefix before row y + 1
-        if (kBand && y + 1 == e) carry_out[static_cast<size_t>(x) * nd + k] = C;
+        if (kBand && y + 1 == e) carry_out[static_cast<size_t>(k - k0) * w + x] = C;
     };
     auto live = [&](int y) { return !kBand || y >= c0; };
     double cur[kPF], nxt[kPF];
@@ -1493,11 +1493,14 @@ void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, in
     launched(ctx, "k_cost_volume");
 }
 
-// A row band's aggregation (DESIGN 7): the packed passes with the vertical
-// prefix seeded from the band above and exported to the band below.
-void aggregate_costs_band(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l,
-                          const uint8_t* r, const uint8_t* u, const uint8_t* d, int max_arm, float* out,
-                          const double* carry_in, int c0, double* carry_out, int e) {
+// A row band's aggregation (DESIGN 7), in two phases so the carry chain
+// covers only the vertical pass: the packed arm words + horizontal pass into
+// the context's scratch, then the vertical pass of slices [k0, k1) with the
+// column prefix seeded from the band above and exported to the band below.
+constexpr int kBandVPF = 8, kBandHPF = 16;
+
+void aggregate_band_hpass(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l, const uint8_t* r,
+                          const uint8_t* u, const uint8_t* d, int max_arm) {
     require(nd >= 1, "aggregate_costs: empty disparity range");
     require(max_arm >= 0 && max_arm <= 127, "row bands: cross_arm_l1 must be <= 127");
     const size_t n = static_cast<size_t>(w) * h;
@@ -1508,24 +1511,38 @@ void aggregate_costs_band(dco_ctx* ctx, const float* cost, int w, int h, int nd,
     dim3 b(32, 8);
     k_region_pack<<<grid2(w, h, b), b, 0, ctx->stream>>>(l, r, u, d, w, h, hinfo, vinfo);
     launched(ctx, "k_region_pack");
-    constexpr int kVPF = 8, kHPF = 16;
-    const int ring_h = 2 * max_arm + 2 + kHPF - 1, ring_v = 2 * max_arm + 2 + kVPF - 1;
+    const int ring_h = 2 * max_arm + 2 + kBandHPF - 1;
     dim3 tb(32, 4);
     const size_t smem_h = static_cast<size_t>(ring_h) * kAggThreads * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_agg_h2<kBandHPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_agg_h2<kBandHPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    k_agg_h2<kBandHPF><<<dim3((nd + 31) / 32, (h + 3) / 4), tb, smem_h, ctx->stream>>>(cost, w, h, nd, hinfo, lag,
+                                                                                      ring_h, hsum);
+    launched(ctx, "k_agg_h2");
+}
+
+void aggregate_band_vpass(dco_ctx* ctx, int w, int h, int nd, int max_arm, float* out, const double* carry_in,
+                          int c0, double* carry_out, int e, int k0, int k1) {
+    require(0 <= k0 && k0 < k1 && k1 <= nd && k0 % 32 == 0, "row bands: slice chunk must start at a multiple of 32");
+    const size_t n = static_cast<size_t>(w) * h;
+    const double* hsum = static_cast<const double*>(scratch(ctx, S_HSUM, n * nd * sizeof(double)));
+    const uint32_t* vinfo = static_cast<const uint32_t*>(scratch(ctx, S_REGION, 2 * n * sizeof(uint32_t))) + n;
+    const int lag = max_arm + 1;
+    const int ring_v = 2 * max_arm + 2 + kBandVPF - 1;
+    dim3 tb(32, 4);
     const size_t smem_v = static_cast<size_t>(ring_v) * kAggThreads * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_agg_v2<kVPF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(k_agg_v2<kVPF, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_agg_v2<kBandVPF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_agg_v2<kBandVPF, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
-    k_agg_h2<kHPF><<<dim3((nd + 31) / 32, (h + 3) / 4), tb, smem_h, ctx->stream>>>(cost, w, h, nd, hinfo, lag,
-                                                                                  ring_h, hsum);
-    launched(ctx, "k_agg_h2");
-    k_agg_v2<kVPF, true><<<dim3((nd + 31) / 32, (w + 3) / 4), tb, smem_v, ctx->stream>>>(
-        hsum, w, h, nd, vinfo, lag, ring_v, out, carry_in, c0, carry_out, e);
+    k_agg_v2<kBandVPF, true><<<dim3((k1 - k0 + 31) / 32, (w + 3) / 4), tb, smem_v, ctx->stream>>>(
+        hsum, w, h, nd, vinfo, lag, ring_v, out, carry_in, c0, carry_out, e, k0, k1);
     launched(ctx, "k_agg_v2_band");
 }
 

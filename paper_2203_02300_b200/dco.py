@@ -236,6 +236,40 @@ def stereo_band(left_sub, right_sub, band, cfg: Config, full_width, full_height,
     return disp, sparse, carry_out
 
 
+def stereo_band_begin(left_sub, right_sub, band, cfg: Config, full_width, full_height):
+    """dco_stereo_band_begin: cross windows, cost and horizontal pass of a band
+    (state stays in this context until stereo_band_end)."""
+    qw = full_width // 2
+    if tuple(left_sub.shape) != (band.sub1 - band.sub0, qw) or left_sub.shape != right_sub.shape:
+        raise InputError("stereo_band: sub-images must be (sub1 - sub0, full_width // 2)")
+    _call(_lib().dco_stereo_band_begin, _p(left_sub), _p(right_sub), ctypes.byref(band), ctypes.byref(cfg),
+          full_width, full_height)
+
+
+def stereo_band_vpass(band, cfg: Config, full_width, full_height, d0, d1, carry_in=None):
+    """dco_stereo_band_vpass over slices [d0, d1): returns the chunk's carry for
+    the band below (or None). Carries are (d1 - d0) x (full_width // 2) doubles."""
+    qw = full_width // 2
+    if carry_in is not None and (carry_in.dtype != torch.float64 or carry_in.numel() != (d1 - d0) * qw):
+        raise InputError("stereo_band_vpass: carry_in must hold (d1 - d0) * (full_width // 2) doubles")
+    carry_out = None
+    if band.carry_out_row >= 0:
+        carry_out = torch.empty(((d1 - d0), qw), dtype=torch.float64, device="cuda")
+    _call(_lib().dco_stereo_band_vpass, ctypes.byref(band), ctypes.byref(cfg), full_width, full_height, d0, d1,
+          _p(carry_in), _p(carry_out))
+    return carry_out
+
+
+def stereo_band_end(band, cfg: Config, full_width, full_height):
+    """dco_stereo_band_end: (disparity rows [row0, row1), sparse full rows [frow0, frow1))."""
+    qw = full_width // 2
+    disp = _f32((band.row1 - band.row0, qw))
+    sparse = _f32((band.frow1 - band.frow0, full_width))
+    _call(_lib().dco_stereo_band_end, ctypes.byref(band), ctypes.byref(cfg), full_width, full_height, _p(disp),
+          _p(sparse))
+    return disp, sparse
+
+
 # ------------------------------------------------------------------ flow ---
 def compute_flow(frm, to, cfg: Config):
     """compute_flow, flow.cpp:185-205: (u, v)."""

@@ -149,6 +149,9 @@ SIGNATURES = {
         [c_void_p, P, P, P, c_int, c_int, P, P, c_int, c_int, c_int, c_int, CFG, c_double, ctypes.POINTER(System),
          ctypes.POINTER(c_uint64), ctypes.POINTER(c_double)],
     ),
+    "dco_stereo_band_begin": (c_int, [c_void_p, P, P, ctypes.POINTER(Band), CFG, c_int, c_int]),
+    "dco_stereo_band_vpass": (c_int, [c_void_p, ctypes.POINTER(Band), CFG, c_int, c_int, c_int, c_int, P, P]),
+    "dco_stereo_band_end": (c_int, [c_void_p, ctypes.POINTER(Band), CFG, c_int, c_int, P, P]),
     "dco_band_solver_create": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_void_p)]),
     "dco_band_solver_destroy": (None, [c_void_p]),
     "dco_band_solver_export": (c_int, [c_void_p, c_void_p]),

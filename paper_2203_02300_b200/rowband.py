@@ -37,11 +37,12 @@ class LocalLinks:
         self.owned = list(range(bands))
         self._carry = {}
 
-    def put_carry(self, k, t):
-        self._carry[k + 1] = t
+    def put_carry(self, key, t):
+        k, d0 = key
+        self._carry[(k + 1, d0)] = t
 
-    def get_carry(self, k, like):
-        return self._carry.pop(k)
+    def get_carry(self, key, like):
+        return self._carry.pop(key)
 
     def gather_stats(self, stats):
         return [stats[k] for k in range(self.bands)]
@@ -60,12 +61,12 @@ class DistLinks:
         self.owned = [rank]
         self.device = device
 
-    def put_carry(self, k, t):
-        self.dist.send(t, dst=k + 1)
+    def put_carry(self, key, t):
+        self.dist.send(t, dst=key[0] + 1)
 
-    def get_carry(self, k, like):
+    def get_carry(self, key, like):
         t = torch.empty_like(like)
-        self.dist.recv(t, src=k - 1)
+        self.dist.recv(t, src=key[0] - 1)
         return t
 
     def gather_stats(self, stats):
@@ -84,8 +85,11 @@ class RowBandFrames:
     """The row-band frame loop of one stream: owns the band plans, the band
     solvers and the previous dense rows (the d_pre chain, pipeline.cpp:133,235)."""
 
-    def __init__(self, full_w, full_h, cfg: Config, links):
+    def __init__(self, full_w, full_h, cfg: Config, links, chunk=None):
+        """chunk: slices per carry message (a multiple of 32); default 32 with
+        one band per rank, the whole range when all bands share this GPU."""
         self.fw, self.fh, self.cfg, self.links = full_w, full_h, cfg, links
+        self.chunk = chunk if chunk is not None else (32 if isinstance(links, DistLinks) else None)
         g = links.bands
         self.plans = {k: dco.band_plan(cfg, full_w, full_h, g, k) for k in links.owned}
         self.solvers = {}
@@ -142,17 +146,25 @@ class RowBandFrames:
         edges, m_i = dco.extract_depth_contours_prefiltered(dco.gaussian_blur(mid_gray, cfg.gauss_sigma), m_fuse, cfg)
         qw = m_fuse.shape[1]
         self._mark("flow+contour")
-        # stereo per band, carries down the chain
+        # stereo per band: only the vertical pass waits for the band above, and
+        # its carry travels in chunks of slices, so band k+1's vertical pass of
+        # chunk c overlaps band k's chunk c+1 (a pipeline, not a serial chain)
         sparse = {}
+        nd = cfg.d_max - cfg.d_min + 1
+        step = self.chunk or nd
+        chunks = [(d0, min(nd, d0 + step)) for d0 in range(0, nd, step)]
         for k in sorted(self.plans):
             b = self.plans[k]
-            carry = None
-            if b.carry_row > 0:
-                carry = L.get_carry(k, torch.empty(dco.band_carry_elems(cfg, fw), dtype=torch.float64, device="cuda"))
-            _, sparse[k], carry_out = dco.stereo_band(mid_q[b.sub0:b.sub1].contiguous(),
-                                                      right_q[b.sub0:b.sub1].contiguous(), b, cfg, fw, fh, carry)
-            if carry_out is not None:
-                L.put_carry(k, carry_out)
+            dco.stereo_band_begin(mid_q[b.sub0:b.sub1].contiguous(), right_q[b.sub0:b.sub1].contiguous(), b, cfg,
+                                  fw, fh)
+            for d0, d1 in chunks:
+                carry = None
+                if b.carry_row > 0:
+                    carry = L.get_carry((k, d0), torch.empty((d1 - d0, fw // 2), dtype=torch.float64, device="cuda"))
+                carry_out = dco.stereo_band_vpass(b, cfg, fw, fh, d0, d1, carry)
+                if carry_out is not None:
+                    L.put_carry((k, d0), carry_out)
+            _, sparse[k] = dco.stereo_band_end(b, cfg, fw, fh)
         self._mark("stereo")
         # frame-wide sparse mean from the bands' exact partials
         stats = {k: self._sparse_stats(sparse[k]) for k in self.plans}

@@ -72,9 +72,9 @@ def _band_links_worker(rank, world, port, out):
     like = torch.empty(6, dtype=torch.float64)
     got = None
     if rank > 0:
-        got = links.get_carry(rank, like).tolist()
+        got = links.get_carry((rank, 0), like).tolist()
     if rank + 1 < world:
-        links.put_carry(rank, torch.arange(6, dtype=torch.float64) + 10.0 * rank)
+        links.put_carry((rank, 0), torch.arange(6, dtype=torch.float64) + 10.0 * rank)
     stats = links.gather_stats({rank: [1.0 + rank, 2.0 * rank, 3.0, -24.0 - rank]})
     blobs = links.gather_bytes({rank: bytes([rank]) * 128})
     g.close()

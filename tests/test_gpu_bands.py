@@ -105,3 +105,31 @@ def test_carry_is_the_exact_column_prefix(gpu, ref):
         gpu.stereo_band(T(lq[b1.sub0:b1.sub1]), T(rq[b1.sub0:b1.sub1]), b1, cfg, fw, fh, carry_in=None)
     with pytest.raises(InputError):
         gpu.stereo_band(T(lq[b1.sub0:b1.sub1 - 1]), T(rq[b1.sub0:b1.sub1 - 1]), b1, cfg, fw, fh, carry_in=carry)
+
+
+@pytest.mark.parametrize("chunk", [32, 64])
+def test_phased_chunked_carry_equals_one_call(gpu, ref, chunk):
+    """begin / vpass per slice chunk / end, carries per chunk: the same bits as
+    the one-call band and the whole frame."""
+    fw, fh, bands = 640, 480, 3
+    cfg = Config(d_max=95)
+    f = scene(ref, fw, fh, seed=13)
+    lq, rq = ref.downsample_half(f["left"]), ref.downsample_half(f["right"])
+    nd = 96
+    chunks = [(d0, min(nd, d0 + chunk)) for d0 in range(0, nd, chunk)]
+    carries, disp = {}, []
+    for k in range(bands):
+        b = gpu.band_plan(cfg, fw, fh, bands, k)
+        gpu.stereo_band_begin(T(lq[b.sub0:b.sub1]), T(rq[b.sub0:b.sub1]), b, cfg, fw, fh)
+        for d0, d1 in chunks:
+            out = gpu.stereo_band_vpass(b, cfg, fw, fh, d0, d1, carries.get((k, d0)) if b.carry_row > 0 else None)
+            if out is not None:
+                carries[(k + 1, d0)] = out
+        d, _ = gpu.stereo_band_end(b, cfg, fw, fh)
+        disp.append(N(d))
+    whole, _ = gpu.stereo_sparse_depth(T(lq), T(rq), cfg, fw, fh)
+    assert bits_equal(np.concatenate(disp), N(whole))
+    with pytest.raises(InputError):  # chunks start at multiples of 32
+        b = gpu.band_plan(cfg, fw, fh, bands, 0)
+        gpu.stereo_band_begin(T(lq[b.sub0:b.sub1]), T(rq[b.sub0:b.sub1]), b, cfg, fw, fh)
+        gpu.stereo_band_vpass(b, cfg, fw, fh, 16, 48)

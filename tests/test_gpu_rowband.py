@@ -15,13 +15,14 @@ from tests.test_gpu_stereo import N, T, bits_equal
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("bands", [1, 2, 3, 5])
-def test_rowband_frames_match_reference(gpu, ref, bands):
+@pytest.mark.parametrize("bands,chunk", [(1, None), (2, None), (3, 32), (5, 64)])
+def test_rowband_frames_match_reference(gpu, ref, bands, chunk):
+    """chunk: the carry travels in slice chunks (as under torchrun)."""
     W, H = 640, 360
     cfg = Config(d_max=47)
     fs = [scene(ref, W, H, index=i, seed=91) for i in range(5)]
     q = [ref.downsample_half(f["left"]) for f in fs]
-    rb = RowBandFrames(W, H, cfg, LocalLinks(bands))
+    rb = RowBandFrames(W, H, cfg, LocalLinks(bands), chunk=chunk)
     prev = None
     for i in range(1, 4):
         mid = fs[i]
