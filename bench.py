@@ -496,7 +496,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=4, help="concurrent pipeline streams per GPU")
+    ap.add_argument("--streams", type=int, default=6, help="concurrent pipeline streams per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
