@@ -149,6 +149,16 @@ int dco_stereo_sparse_depth(dco_ctx* ctx, const float* left_q, const float* righ
                             const dco_config* cfg, int full_w, int full_h, float* disparity,
                             float* sparse);
 
+/* Left-right consistency -- opt-in, not part of the reference (SPEC.md
+ * "Non-goals: no left-right cross-checking"). The right view's disparity is the
+ * stereo chain on the mirrored pair: dco_flip_horizontal both quarter images,
+ * run with left' = mirror(right), right' = mirror(left), mirror the result
+ * back. dco_lr_consistency keeps d_L(x) where the right view at x - d_L agrees
+ * within max_diff, NaN (nodata) elsewhere. */
+int dco_flip_horizontal(dco_ctx* ctx, const float* img, int w, int h, float* out);
+int dco_lr_consistency(dco_ctx* ctx, const float* disp_left, const float* disp_right, int w, int h, double max_diff,
+                       float* out);
+
 /* ---- flow (flow.hpp:35-50) --------------------------------------------- */
 /* compute_flow, flow.cpp:185-205 (pyramid, upsample, DIS patch search). */
 int dco_compute_flow(dco_ctx* ctx, const float* from, const float* to, int w, int h,
@@ -306,6 +316,9 @@ enum {
     DCO_SPAN_COMPOSITE,  /* rendering (composite)                         */
     DCO_SPAN_COUNT
 };
+/* Opt-in left-right consistency on every frame's disparity before the sparse
+ * map (not in the reference; default off): see dco_lr_consistency. */
+int dco_stream_set_lr_check(dco_stream* s, int enable, double max_diff);
 /* Enables (and resets) timing; events ride the stream, no host waits. */
 int dco_stream_set_timing(dco_stream* s, int enable);
 /* Sum of each span's milliseconds over the timed frames (synchronises). */

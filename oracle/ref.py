@@ -369,3 +369,31 @@ def pipeline_frame(past_q, mid_q, future_q, mid_gray, right_q, mid_rgb, d_pre, v
         _check(st)
     return {"dense": dense, "composite": comp, "mask": mask, "edges": edges, "sparse": sparse,
             "iterations": it.value, "objective": obj.value, "unsolvable": st == 3}
+
+
+def lr_consistency(disp_left, disp_right, max_diff=1.0):
+    """Left-right consistency restated in numpy (the reference has none:
+    SPEC.md "Non-goals: no left-right cross-checking"; this is the north_star's
+    opt-in filter). Keeps d_L(x, y) where x_r = x - round(d_L) lies in the map
+    and |d_L - d_R(x_r, y)| <= max_diff (float64 compare); NaN elsewhere."""
+    dl = np.asarray(disp_left, np.float32)
+    dr = np.asarray(disp_right, np.float32)
+    h, w = dl.shape
+    out = np.full((h, w), np.nan, np.float32)
+    ys, xs = np.nonzero(np.isfinite(dl))
+    d = dl[ys, xs]
+    xr = xs - np.floor(d + np.float32(0.5)).astype(np.int64)
+    ok = (xr >= 0) & (xr < w)
+    ys, xs, d, xr = ys[ok], xs[ok], d[ok], xr[ok]
+    e = dr[ys, xr]
+    keep = np.isfinite(e) & (np.abs(d.astype(np.float64) - e.astype(np.float64)) <= max_diff)
+    out[ys[keep], xs[keep]] = d[keep]
+    return out
+
+
+def stereo_disparity(left_q, right_q, cfg):
+    """The reference's stereo chain (stereo.cpp:106-299) on quarter images."""
+    arms = build_cross_windows(left_q, cfg)
+    vol = compute_cost_volume(left_q, right_q, arms, cfg)
+    return refine_disparity_histogram(select_disparity_wta(aggregate_costs(vol, arms, cfg.d_min), cfg.d_min), arms,
+                                      cfg.hist_iterations)

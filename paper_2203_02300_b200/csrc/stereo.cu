@@ -1370,6 +1370,38 @@ __global__ void k_sparse_depth(const float* __restrict__ disp, int w, int h, dou
     out[static_cast<size_t>(y) * fw + x] = v;
 }
 
+// ------------------------------------------ left-right consistency (opt-in) --
+// Not in the reference (SPEC.md "Non-goals: no left-right cross-checking");
+// the north_star's optional filter. The right view's disparity is the same
+// chain on the mirrored pair (left' = mirror(right), right' = mirror(left):
+// q' = x' - d in right' is q = x + d in the left image), mirrored back.
+__global__ void k_flip_h(const float* __restrict__ in, int w, int h, float* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    out[static_cast<size_t>(y) * w + x] = in[static_cast<size_t>(y) * w + (w - 1 - x)];
+}
+
+// keep d_L(x) where the right view maps back: x_r = x - d_L (integer-valued
+// disparities), |d_L(x) - d_R(x_r)| <= max_diff; nodata (NaN) otherwise.
+__global__ void k_lr_check(const float* __restrict__ dl, const float* __restrict__ dr, int w, int h,
+                           double max_diff, float* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    const size_t i = static_cast<size_t>(y) * w + x;
+    const float d = dl[i];
+    float v = __int_as_float(0x7fc00000);
+    if (isfinite(d)) {
+        const int xr = x - static_cast<int>(floorf(d + 0.5f));
+        if (xr >= 0 && xr < w) {
+            const float e = dr[static_cast<size_t>(y) * w + xr];
+            if (isfinite(e) && fabs(static_cast<double>(d) - static_cast<double>(e)) <= max_diff) v = d;
+        }
+    }
+    out[i] = v;
+}
+
 __global__ void k_max_arm(const uint8_t* __restrict__ a0, const uint8_t* __restrict__ a1,
                           const uint8_t* __restrict__ a2, const uint8_t* __restrict__ a3, size_t n,
                           int* __restrict__ out) {
@@ -1742,6 +1774,18 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     }
 }
 
+void flip_horizontal(dco_ctx* ctx, const float* img, int w, int h, float* out) {
+    dim3 b(32, 8);
+    k_flip_h<<<grid2(w, h, b), b, 0, ctx->stream>>>(img, w, h, out);
+    launched(ctx, "k_flip_h");
+}
+
+void lr_consistency(dco_ctx* ctx, const float* dl, const float* dr, int w, int h, double max_diff, float* out) {
+    dim3 b(32, 8);
+    k_lr_check<<<grid2(w, h, b), b, 0, ctx->stream>>>(dl, dr, w, h, max_diff, out);
+    launched(ctx, "k_lr_check");
+}
+
 void disparity_to_sparse_depth(dco_ctx* ctx, const float* disp, int w, int h, const dco_config* cfg,
                                int fw, int fh, float* out) {
     if (fw < w * 2 || fh < h * 2)
@@ -1809,6 +1853,23 @@ int dco_refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h
 int dco_disparity_to_sparse_depth(dco_ctx* ctx, const float* disp, int w, int h, const dco_config* cfg,
                                   int fw, int fh, float* out) {
     return guarded(ctx, [&] { disparity_to_sparse_depth(ctx, disp, w, h, cfg, fw, fh, out); });
+}
+
+int dco_flip_horizontal(dco_ctx* ctx, const float* img, int w, int h, float* out) {
+    return guarded(ctx, [&] {
+        require(w >= 1 && h >= 1, "flip_horizontal: empty image");
+        require(img != out, "flip_horizontal: in-place flip is not supported");
+        flip_horizontal(ctx, img, w, h, out);
+    });
+}
+
+int dco_lr_consistency(dco_ctx* ctx, const float* disp_left, const float* disp_right, int w, int h, double max_diff,
+                       float* out) {
+    return guarded(ctx, [&] {
+        require(w >= 1 && h >= 1, "lr_consistency: empty map");
+        require(max_diff >= 0.0, "lr_consistency: negative tolerance");
+        lr_consistency(ctx, disp_left, disp_right, w, h, max_diff, out);
+    });
 }
 
 }  // extern "C"

@@ -39,6 +39,8 @@ void wta_slices(dco_ctx* ctx, const float* agg, int w, int h, int d_min, int nd,
 void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
                                 const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters, int bin_bound,
                                 int max_arm, float* out);
+void flip_horizontal(dco_ctx* ctx, const float* img, int w, int h, float* out);
+void lr_consistency(dco_ctx* ctx, const float* dl, const float* dr, int w, int h, double max_diff, float* out);
 void disparity_to_sparse_depth(dco_ctx* ctx, const float* disp, int w, int h, const dco_config* cfg, int fw,
                                int fh, float* out);
 void compute_flow_multi(dco_ctx* ctx, const float* from, const float* const* to, int dirs, int w, int h,
@@ -150,6 +152,10 @@ struct dco_stream {
     float* right_q[3];
     float* gray[3];
     float* rgb[3];
+    // opt-in left-right check (not in the reference): mirrored pair, right view, checked map
+    bool lr = false;
+    double lr_max = 1.0;
+    float* lr_buf = nullptr;  // 4 quarter planes
     // per-frame products
     uint8_t* arms;  // 4 planes
     float* cost;
@@ -235,6 +241,29 @@ struct dco_stream {
 
 namespace {
 
+// The stereo chain of the current branch (slice-major or packed exact) on an
+// arbitrary quarter pair into out (the right view of the opt-in LR check).
+void stereo_chain(dco_stream* s, const float* lq, const float* rq, float* out) {
+    dco_ctx* ctx = s->ctx;
+    const dco_config* cfg = &s->cfg;
+    const int qw = s->qw, qh = s->qh;
+    const size_t nq = static_cast<size_t>(qw) * qh;
+    uint8_t *L = s->arms, *R = L + nq, *U = R + nq, *D = U + nq;
+    build_cross_windows(ctx, lq, qw, qh, cfg, L, R, U, D);
+    if (stereo_slices_supported(cfg->cross_arm_l1)) {
+        int* unsafe = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, static_cast<size_t>(s->nd) * sizeof(int)));
+        cost_volume_slices(ctx, lq, rq, qw, qh, L, R, U, D, cfg, cfg->cross_arm_l1, s->cost, unsafe);
+        aggregate_slices(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, unsafe, s->agg);
+        wta_slices(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
+    } else {
+        compute_cost_volume(ctx, lq, rq, qw, qh, L, R, U, D, cfg, s->cost);
+        aggregate_costs(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, s->agg);
+        select_disparity_wta(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
+    }
+    refine_disparity_histogram(ctx, s->disp_wta, qw, qh, L, R, U, D, cfg->hist_iterations, cfg->d_max,
+                               cfg->cross_arm_l1, out);
+}
+
 void run_frame(dco_stream* s, dco_frame_result* res) {
     dco_ctx* ctx = s->ctx;
     const dco_config* cfg = &s->cfg;
@@ -270,6 +299,18 @@ void run_frame(dco_stream* s, dco_frame_result* res) {
     s->mark(DCO_SPAN_WTA + 1);
     refine_disparity_histogram(ctx, s->disp_wta, qw, qh, L, R, U, D, cfg->hist_iterations, cfg->d_max,
                                cfg->cross_arm_l1, s->disparity);
+    if (s->lr) {  // opt-in: right view on the mirrored pair, then the check (counted in the refine span)
+        float* fl = s->lr_buf;
+        float* fr = fl + nq;
+        float* dm = fr + nq;
+        float* dr = dm + nq;
+        flip_horizontal(ctx, s->right_q[mid], qw, qh, fl);
+        flip_horizontal(ctx, s->left_q[mid], qw, qh, fr);
+        stereo_chain(s, fl, fr, dm);
+        flip_horizontal(ctx, dm, qw, qh, dr);
+        lr_consistency(ctx, s->disparity, dr, qw, qh, s->lr_max, dm);
+        cuda_check(cudaMemcpyAsync(s->disparity, dm, nq * 4, cudaMemcpyDeviceToDevice, ctx->stream), "lr copy");
+    }
     s->mark(DCO_SPAN_REFINE + 1);
     disparity_to_sparse_depth(ctx, s->disparity, qw, qh, cfg, fw, fh, s->sparse);
     s->mark(DCO_SPAN_SPARSE + 1);
@@ -543,6 +584,16 @@ int dco_stream_push_gray8_host(dco_stream* s, const uint8_t* left8, const uint8_
                 cuda_check(cudaMemcpyAsync(dense_out, s->dense, nf * 4, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
         }
         cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int dco_stream_set_lr_check(dco_stream* s, int enable, double max_diff) {
+    if (!s) return DCO_INPUT;
+    return guarded(s->ctx, [&] {
+        require(max_diff >= 0.0, "stream: negative left-right tolerance");
+        if (enable && !s->lr_buf) s->lr_buf = s->alloc<float>(4 * static_cast<size_t>(s->qw) * s->qh);
+        s->lr = enable != 0;
+        s->lr_max = max_diff;
     });
 }
 

@@ -198,6 +198,36 @@ def stereo_sparse_depth(left_q, right_q, cfg: Config, full_width, full_height):
     return disp, sparse
 
 
+def flip_horizontal(img):
+    """Mirror a float map left-right."""
+    w, h = _hw(img)
+    out = _f32((h, w))
+    _call(_lib().dco_flip_horizontal, _p(img), w, h, _p(out))
+    return out
+
+
+def lr_consistency(disp_left, disp_right, max_diff=1.0):
+    """Left-right consistency (opt-in; the reference applies none, SPEC.md
+    Non-goals): d_L where the right view agrees within max_diff, else NaN."""
+    w, h = _hw(disp_left)
+    if tuple(disp_right.shape) != (h, w):
+        raise InputError("lr_consistency: disparity maps differ in size")
+    out = _f32((h, w))
+    _call(_lib().dco_lr_consistency, _p(disp_left), _p(disp_right), w, h, float(max_diff), _p(out))
+    return out
+
+
+def stereo_sparse_depth_lr(left_q, right_q, cfg: Config, full_width, full_height, max_diff=1.0):
+    """The stereo chain with the opt-in left-right check before the sparse map:
+    (checked disparity, sparse, left disparity, right disparity)."""
+    d_left, _ = stereo_sparse_depth(left_q, right_q, cfg, full_width, full_height)
+    d_mirror, _ = stereo_sparse_depth(flip_horizontal(right_q), flip_horizontal(left_q), cfg, full_width,
+                                      full_height)
+    d_right = flip_horizontal(d_mirror)
+    checked = lr_consistency(d_left, d_right, max_diff)
+    return checked, disparity_to_sparse_depth(checked, cfg, full_width, full_height), d_left, d_right
+
+
 # ------------------------------------------------------------- row bands ---
 def band_plan(cfg: Config, full_width, full_height, bands, index):
     """dco_band_plan: the quarter rows band `index` of `bands` owns, computes
@@ -688,6 +718,11 @@ class Stream:
 
     SPANS = ["ingest", "cross", "cost", "aggregate", "wta", "refine", "sparse", "flow", "fusion", "box",
              "normalize", "blur", "contour", "assemble", "solve", "composite"]
+
+    def set_lr_check(self, enable=True, max_diff=1.0):
+        """Opt-in left-right consistency before the sparse map (not in the
+        reference; default off)."""
+        native.check(self.ctx, _lib().dco_stream_set_lr_check(self.handle, int(enable), float(max_diff)))
 
     def set_timing(self, enable=True):
         native.check(self.ctx, self.lib.dco_stream_set_timing(self.handle, 1 if enable else 0))

@@ -112,6 +112,8 @@ SIGNATURES = {
     "dco_refine_disparity_histogram": (c_int, [c_void_p, P, c_int, c_int, P, P, P, P, c_int, P]),
     "dco_disparity_to_sparse_depth": (c_int, [c_void_p, P, c_int, c_int, CFG, c_int, c_int, P]),
     "dco_stereo_sparse_depth": (c_int, [c_void_p, P, P, c_int, c_int, CFG, c_int, c_int, P, P]),
+    "dco_flip_horizontal": (c_int, [c_void_p, P, c_int, c_int, P]),
+    "dco_lr_consistency": (c_int, [c_void_p, P, P, c_int, c_int, c_double, P]),
     "dco_compute_flow": (c_int, [c_void_p, P, P, c_int, c_int, CFG, P, P]),
     "dco_flow_to_polar": (c_int, [c_void_p, P, P, c_int, c_int, P, P]),
     "dco_gradient_amplitude": (c_int, [c_void_p, P, c_int, c_int, P]),
@@ -172,6 +174,7 @@ SIGNATURES = {
     "dco_stream_push_f32": (c_int, [c_void_p, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_push_gray8_host": (c_int, [c_void_p, P, P, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_views": (c_int, [c_void_p, ctypes.POINTER(FrameViews)]),
+    "dco_stream_set_lr_check": (c_int, [c_void_p, c_int, c_double]),
     "dco_stream_set_timing": (c_int, [c_void_p, c_int]),
     "dco_stream_span_times": (c_int, [c_void_p, ctypes.POINTER(c_double), ctypes.POINTER(c_uint64)]),
     "dco_stream_state_size": (c_size_t, [c_void_p]),

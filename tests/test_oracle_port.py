@@ -153,3 +153,22 @@ def test_port_stereo_kat(port, ref):
     truth = np.where(f["gt_depth"][valid] == 1.0, 24.0, 12.0)
     assert valid.sum() == 74781
     assert "%.6f" % ((np.abs(dq - truth) <= 1.0).sum() / valid.sum()) == "0.993448"
+
+
+def test_lr_consistency_restatement():
+    """oracle/ref.lr_consistency on a hand-made pair: a fronto-parallel plane at
+    d=2 agrees everywhere x - 2 is inside the map; a disagreeing right view, a
+    NaN and an out-of-map match drop out; max_diff is inclusive."""
+    from oracle import ref
+
+    dl = np.full((2, 6), 2.0, np.float32)
+    dr = np.full((2, 6), 2.0, np.float32)
+    dl[0, 5] = np.nan
+    dr[1, 2] = 3.0   # right view of (1, 4) disagrees by 1
+    out = ref.lr_consistency(dl, dr, 0.5)
+    want = np.full((2, 6), np.nan, np.float32)
+    want[0, 2:5] = 2.0
+    want[1, 2:4] = 2.0
+    want[1, 5] = 2.0
+    assert np.array_equal(np.isnan(out), np.isnan(want)) and np.array_equal(out[~np.isnan(out)], want[~np.isnan(want)])
+    assert np.isfinite(ref.lr_consistency(dl, dr, 1.0)[1, 4])  # |2 - 3| <= 1 keeps it
