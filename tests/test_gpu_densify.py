@@ -193,3 +193,28 @@ def test_stream_matches_reference_pipeline(gpu, ref):
         assert ((mask == want["mask"]) | close).all()
         prev = want["dense"]
     s.close()
+
+
+@pytest.mark.parametrize("w,h", [(1, 1), (1, 9), (9, 1), (2, 3)])
+def test_densify_edge_shapes(gpu, ref, w, h):
+    """assemble (bit-exact) and solve (tolerance) on 1-pixel-wide and tiny
+    systems: no right or down couplings, a single anchor."""
+    cfg = Config(solver_tol=1e-12, solver_max_iter=500)
+    rng = Rng(w * 13 + h)
+    sparse = np.full((h, w), np.nan, np.float32)
+    sparse[0, 0] = 1.5
+    if w * h > 2:
+        sparse[h - 1, w - 1] = 2.5
+    edges = np.zeros((h, w), np.uint8)
+    m_i = np.array([[rng.uniform() for _ in range(w)] for _ in range(h)], np.float32)
+    m_fuse = np.array([[rng.uniform() for _ in range(max(w // 2, 1))] for _ in range(max(h // 2, 1))], np.float32)
+    want_sys = ref.assemble_system(sparse, edges, m_fuse, m_i, None, cfg)
+    sys = gpu.assemble_system(T(sparse), T(edges), T(m_fuse), T(m_i), None, cfg)
+    got = gpu_sys_arrays(sys)
+    for k in ("diag", "coup_h", "coup_v", "rhs", "initial", "anchored"):
+        assert bits_equal(got[k], want_sys[k]), k
+    want, st = ref.solve_dense_depth(want_sys, cfg)
+    dense, gst = gpu.solve_dense_depth(sys, cfg)
+    d = np.abs(N(dense).astype(np.float64) - want)
+    assert d.max() <= MAX_ABS
+    assert abs(gst.iterations - st["iterations"]) <= 2

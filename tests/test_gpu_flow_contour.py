@@ -156,3 +156,24 @@ def test_contour_scene_kat(gpu, ref):
     assert "%.6f" % recall == "1.000000"
     assert "%.6f" % suppression == "0.982492"
     assert int(tex.sum()) == 10738
+
+
+@pytest.mark.parametrize("w,h", [(2, 2), (3, 5), (17, 2), (64, 3), (5, 64)])
+def test_contour_stages_edge_shapes(gpu, ref, w, h):
+    """Gaussian (5 taps, clamped borders wider than the image), Sobel/NMS on
+    1-3 pixel wide maps, the depth gate on a 1-row m_fuse, box filter radii
+    beyond the image (contour.cpp:108-285): bit-exact on ragged shapes."""
+    cfg = Config(t_high=0.3, t_low=0.1)
+    gray = random_image(w, h, 100 + w + 7 * h)
+    gray[:, : w // 2] += 0.3  # an edge to find
+    m_fuse = random_image(max(w // 2, 1), max(h // 2, 1), 5 + w)
+    blurred = ref.gaussian_blur(gray, cfg.gauss_sigma)
+    assert bits_equal(N(gpu.gaussian_blur(T(gray), cfg.gauss_sigma)), blurred)
+    edges, m_i = ref.extract_depth_contours_prefiltered(blurred, m_fuse, cfg)
+    ge, gm = gpu.extract_depth_contours_prefiltered(T(blurred), T(m_fuse), cfg)
+    assert bits_equal(N(gm), m_i) and bits_equal(N(ge), edges)
+    for r in (1, 5, 40):
+        assert bits_equal(N(gpu.box_filter(T(m_fuse), r)), ref.box_filter(m_fuse, r))
+    with pytest.raises(InputError):  # contour.cpp:109, as the reference
+        gpu.box_filter(T(m_fuse), 0)
+    assert bits_equal(N(gpu.normalize_amplitude(T(m_fuse))), ref.normalize_amplitude(m_fuse))
