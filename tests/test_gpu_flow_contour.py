@@ -177,3 +177,15 @@ def test_contour_stages_edge_shapes(gpu, ref, w, h):
     with pytest.raises(InputError):  # contour.cpp:109, as the reference
         gpu.box_filter(T(m_fuse), 0)
     assert bits_equal(N(gpu.normalize_amplitude(T(m_fuse))), ref.normalize_amplitude(m_fuse))
+
+
+@pytest.mark.parametrize("w,h", [(16, 16), (16, 41), (37, 16), (100, 17), (33, 70)])
+def test_flow_ragged_shapes(gpu, ref, w, h):
+    """compute_flow (flow.cpp:29-205) on sizes at the level threshold and with
+    patch grids whose last patch is pinned to the border: bit-exact."""
+    cfg = Config()
+    a = random_image(w, h, 3 * w + h)
+    b = np.roll(a, (1, 2), axis=(0, 1)).astype(np.float32)
+    u, v = ref.compute_flow(a, b, cfg)
+    gu, gv = gpu.compute_flow(T(a), T(b), cfg)
+    assert bits_equal(N(gu), u) and bits_equal(N(gv), v)
