@@ -140,6 +140,11 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
     // the rest in registers
     constexpr int XT = (64 - 8 * EPT) / 2 < EPT ? (64 - 8 * EPT) / 2 : EPT;
     const uint32_t tmx = tm + 8 * EPT;
+    if (a.dbg && t == 0 && blockIdx.x == 0) {  // globaltimer: setup / teardown split (DCO_PCG_DEBUG)
+        unsigned long long gt_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+        a.dbg[6] = static_cast<long long>(gt_);
+    }
     const double cterm = a.constant_term_dev ? *a.constant_term_dev : a.constant_term_host;
 
     // setup (densify.cpp:147-166): x = initial, r = b - A x, z = M r, p = z
@@ -191,6 +196,11 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
         }
     }
     barrier_reduce<5>(tot, bar, a.part, gen, sm, tot);
+    if (a.dbg && t == 0 && blockIdx.x == 0) {  // globaltimer: setup / teardown split (DCO_PCG_DEBUG)
+        unsigned long long gt_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+        a.dbg[7] = static_cast<long long>(gt_);
+    }
     const double bnorm = sqrt(tot[0]);
     const double denom = bnorm > 0.0 ? bnorm : 1.0;
     double snorm = sqrt(tot[1]);
@@ -419,6 +429,11 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
             ++iter;
         }
     }
+    if (a.dbg && t == 0 && blockIdx.x == 0) {
+        unsigned long long gt_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+        a.dbg[8] = static_cast<long long>(gt_);
+    }
     // publish xs for the final objective's stencil, dense map
     tm_wait_st();
 #pragma unroll
@@ -448,6 +463,11 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
         o[1] += a.rhs[i] * xsi;
     }
     barrier_reduce<2>(o, bar, a.part, gen, sm, o);
+    if (a.dbg && t == 0 && blockIdx.x == 0) {  // globaltimer: setup / teardown split (DCO_PCG_DEBUG)
+        unsigned long long gt_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+        a.dbg[9] = static_cast<long long>(gt_);
+    }
     if (blockIdx.x == 0 && t == 0) {
         a.out->objective_final = o[0] - 2.0 * o[1] + cterm;
         a.out->status = 0;

@@ -24,7 +24,7 @@ mf = dco.view_tensor(v.m_fuse, (H // 2, W // 2), torch.float32).clone()
 mi = dco.view_tensor(v.m_i, (H, W), torch.float32).clone()
 dense = dco.view_tensor(v.dense, (H, W), torch.float32).clone()
 sysm = dco.assemble_system(sparse, edges, mf, mi, dense, cfg)
-for cap in (1, 10, 40, 80):
+for cap in (0, 1, 10, 40, 80):
     c = cfg.copy(solver_max_iter=cap, solver_tol=1e-30)
     for _ in range(2):
         out, st = dco.solve_dense_depth(sysm, c, history_cap=0)

@@ -53,3 +53,7 @@ wm = work.mean(0)
 order = np.argsort(-wm)
 print("slowest blocks:", [(int(b), int(wm[b])) for b in order[:8]])
 print("fastest blocks:", [(int(b), int(wm[b])) for b in order[-4:]])
+# block 0 globaltimer (ns): kernel entry (after the anchor check), after the
+# setup barrier, loop exit, after the final objective barrier
+e = np.array(buf[6:10], dtype=np.float64)
+print("setup ns %.0f  loop ns %.0f  teardown ns %.0f" % (e[1] - e[0], e[2] - e[1], e[3] - e[2]))
