@@ -366,7 +366,6 @@ struct CGArgs {
     const float* fallback;    // unsolvable: dense = fallback (or NaN when null)
     const int* fallback_valid;  // nullable: fallback usable only when *fallback_valid
     SolveOut* out;
-    int mode;  // experiment knobs (0 in production): 1 no in-loop grid sync, 2 no halo loads, 4 no prec load
     long long* dbg;  // optional per-phase clock64 stamps of block 0 (DCO_PCG_DEBUG)
 };
 
@@ -871,7 +870,6 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     a.fallback = fallback;
     a.fallback_valid = fallback_valid;
     a.out = static_cast<SolveOut*>(out_dev);
-    a.mode = getenv("DCO_PCG_MODE") ? atoi(getenv("DCO_PCG_MODE")) : 0;
     a.dbg = nullptr;
     if (getenv("DCO_PCG_DEBUG")) {
         static long long* dbg = nullptr;
