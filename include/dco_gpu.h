@@ -328,6 +328,23 @@ size_t dco_stream_state_size(const dco_stream* s);
 int dco_stream_save_state(dco_stream* s, void* host_buf, size_t len);
 int dco_stream_load_state(dco_stream* s, const void* host_buf, size_t len);
 
+/* ---- ingest / egress (codec.cpp, image.cpp) ------------
+ * quantize (codec.cpp:23-26) and to_gray (image.cpp:7-15) on the device, so
+ * only bytes cross PCIe; the file formats on the host, byte-for-byte the
+ * reference's. The host functions need no context: err (may be NULL)
+ * receives the reference's message, e.g. "<path>: truncated payload (byte
+ * offset N)"; status DCO_CODEC as CodecError. */
+int dco_quantize_u8(dco_ctx* ctx, const float* in, size_t n, uint8_t* out);
+int dco_to_gray(dco_ctx* ctx, const float* rgb, int w, int h, float* gray);
+/* read_pnm (codec.cpp:59-82): P5 (gray) or P6 (expect_color) with maxval 255.
+ * bytes == NULL reads the header only (w, h). */
+int dco_read_pnm(const char* path, int expect_color, uint8_t* bytes, size_t cap, int* w, int* h, char* err,
+                 size_t err_len);
+/* write_pgm / write_ppm (codec.cpp:211-229) of already-quantised bytes. */
+int dco_write_pnm(const char* path, const uint8_t* bytes, int w, int h, int channels, char* err, size_t err_len);
+/* write_pfm (codec.cpp:293-309): rows bottom-up, nodata written as +inf. */
+int dco_write_pfm(const char* path, const float* map, int w, int h, char* err, size_t err_len);
+
 /* ---- row bands (3840x2160 over G GPUs) ------------
  * The quarter-scale rows split into G contiguous bands. Band k computes the
  * stereo chain on its rows plus a recompute halo of (I+1)*l1 + max(Rc,1)

@@ -33,6 +33,11 @@ def lib():
             "ref_load_config": (I, [ctypes.c_char_p, CFG]),
             "ref_render_synth_frame": (I, [I, I, D, D, D, D, I, D, D, D, D, U64, I, P, P, P, P, P, P]),
             "ref_pgm_roundtrip": (I, [P, I, I, ctypes.c_char_p, P, P]),
+            "ref_write_pgm": (I, [P, I, I, ctypes.c_char_p]),
+            "ref_write_ppm": (I, [P, I, I, ctypes.c_char_p]),
+            "ref_write_pfm": (I, [P, I, I, ctypes.c_char_p]),
+            "ref_read_pnm": (I, [ctypes.c_char_p, I, P, ctypes.c_size_t, ctypes.POINTER(I), ctypes.POINTER(I)]),
+            "ref_to_gray": (I, [P, I, I, P]),
             "ref_downsample_half": (I, [P, I, I, P]),
             "ref_build_cross_windows": (I, [P, I, I, CFG, P, P, P, P]),
             "ref_census_transform": (I, [P, I, I, I, I, P]),
@@ -397,3 +402,38 @@ def stereo_disparity(left_q, right_q, cfg):
     vol = compute_cost_volume(left_q, right_q, arms, cfg)
     return refine_disparity_histogram(select_disparity_wta(aggregate_costs(vol, arms, cfg.d_min), cfg.d_min), arms,
                                       cfg.hist_iterations)
+
+
+def write_pgm(img, path):
+    """write_pgm, codec.cpp:211-219."""
+    img = _c(img, np.float32)
+    _check(lib().ref_write_pgm(_p(img), img.shape[1], img.shape[0], path.encode()))
+
+
+def write_ppm(rgb, path):
+    """write_ppm, codec.cpp:221-229."""
+    rgb = _c(rgb, np.float32)
+    _check(lib().ref_write_ppm(_p(rgb), rgb.shape[1], rgb.shape[0], path.encode()))
+
+
+def write_pfm(fmap, path):
+    """write_pfm, codec.cpp:293-309."""
+    fmap = _c(fmap, np.float32)
+    _check(lib().ref_write_pfm(_p(fmap), fmap.shape[1], fmap.shape[0], path.encode()))
+
+
+def read_pnm(path, color=False):
+    """read_pnm, codec.cpp:59-82: the floats (bytes / 255.0f)."""
+    w, h = I(), I()
+    _check(lib().ref_read_pnm(path.encode(), int(color), None, 0, ctypes.byref(w), ctypes.byref(h)))
+    out = np.empty((h.value, w.value, 3) if color else (h.value, w.value), np.float32)
+    _check(lib().ref_read_pnm(path.encode(), int(color), _p(out), out.size, ctypes.byref(w), ctypes.byref(h)))
+    return out
+
+
+def to_gray(rgb):
+    """to_gray, image.cpp:7-15."""
+    rgb = _c(rgb, np.float32)
+    out = np.empty(rgb.shape[:2], np.float32)
+    _check(lib().ref_to_gray(_p(rgb), rgb.shape[1], rgb.shape[0], _p(out)))
+    return out

@@ -258,6 +258,51 @@ int ref_pgm_roundtrip(const float* img, int w, int h, const char* tmp_path, uint
     });
 }
 
+// write_pgm / write_ppm / write_pfm (codec.cpp:211-229, 293-309), read_pnm via
+// read_gray / read_color (codec.cpp:59-82, 199-209), to_gray (image.cpp:7-15).
+int ref_write_pgm(const float* img, int w, int h, const char* path) {
+    return guarded([&] { write_pgm(gray_in(img, w, h), path); });
+}
+
+int ref_write_ppm(const float* rgb, int w, int h, const char* path) {
+    return guarded([&] {
+        ColorImage c(w, h);
+        std::memcpy(c.data.data(), rgb, sizeof(float) * c.data.size());
+        write_ppm(c, path);
+    });
+}
+
+int ref_write_pfm(const float* map, int w, int h, const char* path) {
+    return guarded([&] { write_pfm(map_in(map, w, h), path); });
+}
+
+// read_pnm of a P5 (color = 0) or P6 file; out (may be NULL) receives the
+// floats (bytes / 255.0f), w and h the dimensions.
+int ref_read_pnm(const char* path, int color, float* out, size_t cap, int* w, int* h) {
+    return guarded([&] {
+        LoadedImage img = read_image(path, color ? ImageFormat::Ppm : ImageFormat::Pgm);  // = read_pnm(path, color)
+        if (color) {
+            const ColorImage& c = std::get<ColorImage>(img);
+            *w = c.width;
+            *h = c.height;
+            if (out && cap >= c.data.size()) copy_out(c.data, out);
+        } else {
+            const GrayImage& g = std::get<GrayImage>(img);
+            *w = g.width;
+            *h = g.height;
+            if (out && cap >= g.data.size()) copy_out(g.data, out);
+        }
+    });
+}
+
+int ref_to_gray(const float* rgb, int w, int h, float* out) {
+    return guarded([&] {
+        ColorImage c(w, h);
+        std::memcpy(c.data.data(), rgb, sizeof(float) * c.data.size());
+        copy_out(to_gray(c).data, out);
+    });
+}
+
 // downsample_half, pyramid.cpp:5-17.
 int ref_downsample_half(const float* img, int w, int h, float* out) {
     return guarded([&] { copy_out(downsample_half(gray_in(img, w, h)).data, out); });

@@ -101,6 +101,67 @@ def ingest_gray8(gray8):
     return full, quarter
 
 
+# ------------------------------------------------------ ingest / egress ---
+def quantize_u8(img):
+    """quantize (codec.cpp:23-26) on the device: clamp to [0, 1], lround(v * 255)."""
+    out = torch.empty(img.shape, dtype=torch.uint8, device="cuda")
+    _call(_lib().dco_quantize_u8, _p(img), img.numel(), _p(out))
+    return out
+
+
+def to_gray(rgb):
+    """to_gray (image.cpp:7-15): Rec. 601 luma of an (h, w, 3) float image."""
+    if rgb.dim() != 3 or rgb.shape[2] != 3:
+        raise InputError("to_gray: expected an (h, w, 3) image")
+    h, w = rgb.shape[0], rgb.shape[1]
+    out = _f32((h, w))
+    _call(_lib().dco_to_gray, _p(rgb), w, h, _p(out))
+    return out
+
+
+def _codec(fn, *args):
+    err = ctypes.create_string_buffer(512)
+    st = fn(*args, err, 512)
+    if st != 0:
+        from .config import raise_for
+
+        raise_for(st, err.value.decode() or "codec error %d" % st)
+
+
+def read_pnm(path, color=False):
+    """read_pnm (codec.cpp:59-82): the payload bytes as a host numpy array,
+    (h, w) or (h, w, 3). dco_ingest_gray8 turns gray bytes into read_gray's floats."""
+    import numpy as np
+
+    w, h = ctypes.c_int(), ctypes.c_int()
+    _codec(_lib().dco_read_pnm, path.encode(), int(color), None, 0, ctypes.byref(w), ctypes.byref(h))
+    shape = (h.value, w.value, 3) if color else (h.value, w.value)
+    buf = np.empty(shape, np.uint8)
+    _codec(_lib().dco_read_pnm, path.encode(), int(color), buf.ctypes.data, buf.nbytes, ctypes.byref(w),
+           ctypes.byref(h))
+    return buf
+
+
+def write_pgm(path, img):
+    """write_pgm (codec.cpp:211-219): quantised on the device, 1 byte per pixel over PCIe."""
+    b = quantize_u8(img).cpu().numpy()
+    _codec(_lib().dco_write_pnm, path.encode(), b.ctypes.data, b.shape[1], b.shape[0], 1)
+
+
+def write_ppm(path, rgb):
+    """write_ppm (codec.cpp:221-229) of an (h, w, 3) float image."""
+    b = quantize_u8(rgb).cpu().numpy()
+    _codec(_lib().dco_write_pnm, path.encode(), b.ctypes.data, b.shape[1], b.shape[0], 3)
+
+
+def write_pfm(path, fmap):
+    """write_pfm (codec.cpp:293-309)."""
+    import numpy as np
+
+    a = np.ascontiguousarray(fmap.cpu().numpy() if hasattr(fmap, "cpu") else fmap, np.float32)
+    _codec(_lib().dco_write_pfm, path.encode(), a.ctypes.data, a.shape[1], a.shape[0])
+
+
 # ---------------------------------------------------------------- stereo ---
 @dataclass
 class CrossWindowField:

@@ -140,6 +140,12 @@ SIGNATURES = {
     "dco_composite": (c_int, [c_void_p, P, P, P, P, c_int, c_int, P, P]),
     "dco_transform_mesh": (c_int, [c_void_p, P, c_int, P, P]),
     "dco_render_virtual": (c_int, [c_void_p, P, P, P, c_int, c_double, c_double, c_double, c_int, c_int, P, P]),
+    "dco_quantize_u8": (c_int, [c_void_p, P, c_size_t, P]),
+    "dco_to_gray": (c_int, [c_void_p, P, c_int, c_int, P]),
+    "dco_read_pnm": (c_int, [c_char_p, c_int, c_void_p, c_size_t, ctypes.POINTER(c_int), ctypes.POINTER(c_int),
+                             c_char_p, c_size_t]),
+    "dco_write_pnm": (c_int, [c_char_p, c_void_p, c_int, c_int, c_int, c_char_p, c_size_t]),
+    "dco_write_pfm": (c_int, [c_char_p, c_void_p, c_int, c_int, c_char_p, c_size_t]),
     "dco_band_plan": (c_int, [CFG, c_int, c_int, c_int, c_int, ctypes.POINTER(Band)]),
     "dco_band_carry_bytes": (c_size_t, [CFG, c_int]),
     "dco_stereo_band": (c_int, [c_void_p, P, P, ctypes.POINTER(Band), CFG, c_int, c_int, P, P, P, P]),
