@@ -115,6 +115,11 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
 #define DCO_OK(k) ((k) < nv)
 #define KO(k) ((k) * THREADS)
 
+    if (a.dbg && t == 0 && blockIdx.x == 0) {  // kernel entry (DCO_PCG_DEBUG)
+        unsigned long long gt_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+        a.dbg[636] = static_cast<long long>(gt_);
+    }
     unsigned long long anchors = a.anchors_dev ? *a.anchors_dev : a.anchors_host;
     if (anchors == 0) {
         const float* fb = (a.fallback && (!a.fallback_valid || *a.fallback_valid)) ? a.fallback : nullptr;

@@ -57,3 +57,13 @@ print("fastest blocks:", [(int(b), int(wm[b])) for b in order[-4:]])
 # setup barrier, loop exit, after the final objective barrier
 e = np.array(buf[6:10], dtype=np.float64)
 print("setup ns %.0f  loop ns %.0f  teardown ns %.0f" % (e[1] - e[0], e[2] - e[1], e[3] - e[2]))
+print("entry -> setup start ns %.0f" % (e[0] - buf[636]))
+# the stream's own solve span (CUDA events on its stream, includes launch and k_keep_dense)
+s.set_timing(True)
+for i in range(4, 8):
+    l8, r8 = vid.frame(i)
+    s.push_gray8(torch.from_numpy(l8).cuda(), torch.from_numpy(r8).cuda(), want_result=False)
+spans, nfr = s.span_times()
+lib.dco_debug_pcg_stamps(buf, LEN)
+e = np.array(buf[6:10], dtype=np.float64)
+print("stream solve span ms %.4f; kernel entry->end ms %.4f" % (spans["solve"] / nfr, (e[3] - buf[636]) / 1e6))
