@@ -283,6 +283,14 @@ int dco_stream_set_next_pose(dco_stream* s, const double* pose);
 int dco_stream_push_gray8(dco_stream* s, const uint8_t* left8, const uint8_t* right8,
                           const uint8_t* rgb8, dco_frame_result* result);
 /* Same with float [0,1] inputs (GrayImage/ColorImage data). rgb may be NULL. */
+/* The batched throughput entry point (SURVEY 8b "dco_run_streams"):
+ * frames_per_stream frames for each of n streams, interleaved (frame f of every
+ * stream, then f + 1). left8[k] / right8[k]: frames_per_stream consecutive
+ * device-resident w*h u8 frames of stream k. results (may be NULL):
+ * n * frames_per_stream entries, stream-major; asking for them synchronises
+ * every frame. Errors stop at the failing frame (its stream's error string). */
+int dco_run_streams(dco_stream* const* streams, int n, const uint8_t* const* left8, const uint8_t* const* right8,
+                    int frames_per_stream, dco_frame_result* results);
 int dco_stream_push_f32(dco_stream* s, const float* left, const float* right, const float* rgb,
                         dco_frame_result* result);
 /* Host-buffer variant: H2D of the frame, the full frame pipeline, D2H of the

@@ -540,6 +540,25 @@ int dco_stream_push_gray8(dco_stream* s, const uint8_t* left8, const uint8_t* ri
     });
 }
 
+int dco_run_streams(dco_stream* const* streams, int n, const uint8_t* const* left8, const uint8_t* const* right8,
+                    int frames_per_stream, dco_frame_result* results) {
+    if (!streams || n < 1 || !left8 || !right8 || frames_per_stream < 0) return DCO_INPUT;
+    for (int k = 0; k < n; ++k)
+        if (!streams[k] || !left8[k] || !right8[k]) return DCO_INPUT;
+    // frame f of every stream, then f + 1: each stream's launches go to its own
+    // context stream, so the streams' frames overlap on the device
+    for (int f = 0; f < frames_per_stream; ++f) {
+        for (int k = 0; k < n; ++k) {
+            dco_stream* s = streams[k];
+            const size_t nf = static_cast<size_t>(s->fw) * s->fh;
+            dco_frame_result* r = results ? &results[static_cast<size_t>(k) * frames_per_stream + f] : nullptr;
+            const int st = dco_stream_push_gray8(s, left8[k] + f * nf, right8[k] + f * nf, nullptr, r);
+            if (st != DCO_OK) return st;
+        }
+    }
+    return DCO_OK;
+}
+
 int dco_stream_push_f32(dco_stream* s, const float* left, const float* right, const float* rgb,
                         dco_frame_result* res) {
     if (!s) return DCO_INPUT;

@@ -634,6 +634,33 @@ class BandSolver:
             pass
 
 
+def run_streams(streams, left8, right8, want_results=False):
+    """dco_run_streams: left8[k] / right8[k] are (frames, h, w) u8 CUDA tensors
+    for stream k; all streams advance frame by frame. Returns the per-frame
+    results [k][f] when asked (synchronising), else None."""
+    n = len(streams)
+    if n == 0 or len(left8) != n or len(right8) != n:
+        raise InputError("run_streams: one left and one right batch per stream")
+    frames = left8[0].shape[0]
+    for k, st in enumerate(streams):
+        if tuple(left8[k].shape) != (frames, st.full_h, st.full_w) or left8[k].shape != right8[k].shape:
+            raise InputError("run_streams: batch k must be (frames, h, w) u8 for stream k")
+        if left8[k].dtype != torch.uint8 or right8[k].dtype != torch.uint8:
+            raise InputError("run_streams: u8 frames expected")
+    for st in streams:
+        st._bind()
+    hs = (ctypes.c_void_p * n)(*[st.handle for st in streams])
+    ls = (ctypes.c_void_p * n)(*[_p(t).value for t in left8])
+    rs = (ctypes.c_void_p * n)(*[_p(t).value for t in right8])
+    res = (native.FrameResult * (n * frames))() if want_results else None
+    st = _lib().dco_run_streams(hs, n, ls, rs, frames, res)
+    if st != 0:
+        native.check(streams[0].ctx, st)
+    if not want_results:
+        return None
+    return [[res[k * frames + f] for f in range(frames)] for k in range(n)]
+
+
 def band_connect_local(solvers):
     """All ranks in this process, on this GPU (the emulation of a multi-GPU
     band solve with fewer GPUs than ranks)."""

@@ -177,6 +177,11 @@ SIGNATURES = {
     "dco_stream_set_mesh": (c_int, [c_void_p, P, c_int, P, c_int, P]),
     "dco_stream_set_next_pose": (c_int, [c_void_p, P]),
     "dco_stream_push_gray8": (c_int, [c_void_p, P, P, P, ctypes.POINTER(FrameResult)]),
+    "dco_run_streams": (
+        c_int,
+        [ctypes.POINTER(c_void_p), c_int, ctypes.POINTER(c_void_p), ctypes.POINTER(c_void_p), c_int,
+         ctypes.POINTER(FrameResult)],
+    ),
     "dco_stream_push_f32": (c_int, [c_void_p, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_push_gray8_host": (c_int, [c_void_p, P, P, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_views": (c_int, [c_void_p, ctypes.POINTER(FrameViews)]),
