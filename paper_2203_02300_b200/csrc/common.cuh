@@ -73,6 +73,7 @@ enum Slot : int {
     S_FLAG_PEAK,
     S_FLAG_ASM,
     S_FLAG_SLICE,
+    S_FLAG_DIV,
     S_RENDER,
     S_RENDER_LIST,
     S_HIST,

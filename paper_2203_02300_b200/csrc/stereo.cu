@@ -17,6 +17,10 @@
 
 #include <algorithm>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "dco_exp_table.h"
 #include "dco_libm.h"
@@ -198,9 +202,30 @@ constexpr int kCostPix = 64;  // pixels of one row per cost-volume block
 struct CostParams {
     int w, h, nd, d_min, bits;
     double lambda_ad;
+    double inv_lambda;  // RN(1 / lambda_ad)
+    int fast_div;       // div_lambda proven equal to the division for every |dI| in [0, 1]
     double alpha[256];
     double census[65];
 };
+
+// c / lambda from RN(1/lambda): the product and one FMA correction. For a
+// given lambda the host proves it equal to the IEEE division for every
+// c = |dI| * 255 with |dI| a float in [0, 1] (k_verify_div, all 1.07e9 of
+// them) before enabling it; other inputs take the division.
+__device__ __forceinline__ double div_lambda(double c, double lam, double inv) {
+    const double q = c * inv;
+    return __fma_rn(__fma_rn(-q, lam, c), inv, q);
+}
+
+__global__ void k_verify_div(double lam, double inv, unsigned* __restrict__ bad) {
+    const unsigned n = 0x3f800001u;  // float bit patterns of [0, 1]
+    unsigned miss = 0;
+    for (unsigned u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const double c = static_cast<double>(__uint_as_float(u)) * 255.0;
+        miss |= __double_as_longlong(div_lambda(c, lam, inv)) != __double_as_longlong(c / lam) ? 1u : 0u;
+    }
+    if (__any_sync(0xffffffffu, miss) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
 
 __global__ void __launch_bounds__(512) k_cost_volume(const float* __restrict__ left,
                                                      const float* __restrict__ right,
@@ -241,8 +266,12 @@ __global__ void __launch_bounds__(512) k_cost_volume(const float* __restrict__ l
                 c = 2.0f;
             } else {
                 const size_t q = p - static_cast<size_t>(d);
-                double c_ad = static_cast<double>(fabsf(lum - right[q])) * 255.0;
-                double ad_term = 1.0 - dco_exp(-c_ad / prm->lambda_ad, s_exp);
+                const float adi = fabsf(lum - right[q]);
+                const double c_ad = static_cast<double>(adi) * 255.0;
+                // -c_ad / lambda (stereo.cpp:141): the proven fast quotient inside [0, 1]
+                const double quo = (prm->fast_div && adi <= 1.0f) ? div_lambda(c_ad, prm->lambda_ad, prm->inv_lambda)
+                                                                  : c_ad / prm->lambda_ad;
+                double ad_term = 1.0 - dco_exp(-quo, s_exp);
                 int hd = __popcll(cp ^ cr[q]);
                 c = static_cast<float>(alpha * ad_term + beta * s_census[hd]);
             }
@@ -1501,6 +1530,29 @@ void census_transform(dco_ctx* ctx, const float* img, int w, int h, int ww, int 
     launched(ctx, "k_census");
 }
 
+// Whether div_lambda equals the IEEE division for this lambda over the whole
+// [0, 1] input domain: one exhaustive device check per (device, lambda),
+// cached for the process.
+bool lambda_division_fast(dco_ctx* ctx, double lam) {
+    static std::mutex mu;
+    static std::map<std::pair<int, uint64_t>, bool> known;
+    uint64_t bits;
+    memcpy(&bits, &lam, 8);
+    const auto key = std::make_pair(ctx->device, bits);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = known.find(key);
+    if (it != known.end()) return it->second;
+    unsigned* bad = static_cast<unsigned*>(scratch(ctx, S_FLAG_DIV, 64));
+    cuda_check(cudaMemsetAsync(bad, 0, sizeof(unsigned), ctx->stream), "memset");
+    k_verify_div<<<148 * 8, 256, 0, ctx->stream>>>(lam, 1.0 / lam, bad);
+    launched(ctx, "k_verify_div");
+    unsigned host = 1;
+    cuda_check(cudaMemcpyAsync(&host, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+    known[key] = host == 0;
+    return host == 0;
+}
+
 void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, int w, int h,
                          const uint8_t* l, const uint8_t* r, const uint8_t* u, const uint8_t* d,
                          const dco_config* cfg, float* cost) {
@@ -1515,6 +1567,8 @@ void compute_cost_volume(dco_ctx* ctx, const float* left, const float* right, in
     hp.d_min = cfg->d_min;
     hp.bits = cfg->census_window_w * cfg->census_window_h - 1;
     hp.lambda_ad = cfg->lambda_ad;
+    hp.inv_lambda = 1.0 / cfg->lambda_ad;
+    hp.fast_div = lambda_division_fast(ctx, cfg->lambda_ad) ? 1 : 0;
     StereoTables t;
     make_stereo_tables(cfg, &t);
     for (int i = 0; i < 256; ++i) hp.alpha[i] = t.alpha[i];
