@@ -4,21 +4,28 @@
 A step is one composited frame of the full DCO path for one stream in steady
 state (previous-dense chain active): stereo (cross windows, AD-census cost,
 aggregation, WTA, histogram refinement, sparse depth) + bidirectional flow +
-depth contours + assemble + PCG/MR densify + composite against a rendered
-virtual layer — the body of run_pipeline (reference src/pipeline.cpp:183-258).
+depth contours + assemble + PCG/MR densify + render + composite — the body of
+run_pipeline (reference src/pipeline.cpp:183-258).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One process per GPU (torchrun for N>1); every rank runs --streams independent
+One process per GPU. Under torchrun the ranks come from the environment; a
+plain `python bench.py --gpus N` (N > 1) re-launches itself under
+torch.distributed.run with N ranks. Every rank runs --streams independent
 pipeline streams concurrently (own dco_ctx + CUDA stream each; frames shard
 across streams and GPUs, no data-path collective: "scaling": "weak"). A step
 is one frame on every stream. The timed region is bracketed by a barrier +
 cuda.synchronize; the reported time is the max over ranks. L2 is flushed
-(160 MiB memset; the L2 is 126 MB) before every frame inside the timed region (conservative).
+(160 MiB memset; the L2 is 126 MB) before every frame inside the timed region.
 
 `value` times frames whose u8 inputs are already in HBM. `e2e` times the same
 steps through the host-buffer C-ABI (dco_stream_push_gray8_host): pinned u8
 frames H2D, the pipeline, the composite/mask/dense D2H.
+
+--impl reference runs the reference's own public frame loop, dco::run_pipeline
+(pipeline.cpp:108-321, oracle/_ref built unmodified from /root/reference), on
+one process per host core, each over its own PGM stream with per-frame poses
+and the OBJ cube, timed by the reference's own StageTimings.
 """
 import argparse
 import json
@@ -35,6 +42,29 @@ sys.path.insert(0, ROOT)
 W, H, D = 1280, 720, 128
 NQ, NF = (W // 2) * (H // 2), W * H
 METRIC = "stereo frames/sec at 1280x720 D=128 (1/2/4/8 B200) vs CPU; HBM GB/s fraction"
+STREAMS_PER_GPU = 6
+# the workload, identical in both arms' lines (arm-specific details go under "arm")
+CONFIG = {
+    "workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+render+composite)",
+    "width": W, "height": H, "disparities": D,
+    "frames": "synthetic stereo video (paper_2203_02300_b200.synth), independent streams, d_pre chain active",
+    "virtual_layer": "cube mesh (0.3 m) rendered per frame under a per-frame pose",
+    "l2": "GPU arm: flushed (160 MiB memset, L2 is 126 MB) before every frame, inside the timed region",
+    "parallelism": "frames shard as independent streams: 6 per GPU x N GPUs (GPU arm), one per host core "
+                   "(reference arm); no data-path collective",
+}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def peaks():
@@ -146,104 +176,127 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_reference_frames(frames, d_pre_list, cfg_dict, procs):
-    """Runs the reference pipeline (oracle/_ref) on `procs` processes, one frame
-    each, concurrently. Returns wall seconds."""
-    import multiprocessing as mp
-
-    ctx = mp.get_context("fork")
-    jobs = [(frames[i % len(frames)], d_pre_list[i % len(d_pre_list)], cfg_dict) for i in range(procs)]
-    with ctx.Pool(procs) as pool:
-        pool.map(_cpu_warm, range(procs))
-        t0 = time.perf_counter()
-        pool.map(_cpu_job, jobs)
-        return time.perf_counter() - t0
-
-
-def cpu_procs():
-    """All host threads, bounded by memory (~0.7 GB per reference process)."""
+def cpu_procs(mem_per_proc=0.8e9):
+    """All host threads, bounded by memory (~0.8 GB per reference process at
+    1280x720 D=128)."""
     n = os.cpu_count() or 1
     try:
         import psutil
 
-        n = max(1, min(n, int(psutil.virtual_memory().available / 0.7e9)))
+        n = max(1, min(n, int(psutil.virtual_memory().available / mem_per_proc)))
     except Exception:
         pass
     return n
 
 
-def _cpu_warm(_):
-    from oracle import ref
+def _ref_stream_worker(job, barrier, out_q):
+    """One reference process: writes its stream as PGM frames + manifest (per
+    frame poses) + OBJ cube + config, waits for every process, then runs the
+    reference's dco::run_pipeline over it (oracle/_ref)."""
+    try:
+        from oracle import ref, refseq
+        from paper_2203_02300_b200.config import Config
+        from paper_2203_02300_b200.synth import StereoVideo
 
-    ref.lib()
-    return 0
+        seed, nframes, root, cfg_dict, keep = job
+        vid = StereoVideo(W, H, seed=seed)
+        frames = [vid.frame(i) for i in range(nframes)]
+        paths = refseq.write_sequence(root, frames, poses=[frame_pose(i) for i in range(nframes)],
+                                      mesh=cube_mesh(0.3), cfg=Config(**cfg_dict), keep_outputs=keep)
+        ref.lib()
+        barrier.wait()
+        t0 = time.monotonic()
+        res = ref.run_pipeline(*paths)
+        out_q.put((seed, res, t0, time.monotonic(), paths[2]))
+    except Exception as e:  # report, don't hide
+        out_q.put((job[0], "error: %s" % e, 0.0, 0.0, None))
 
 
-def _cpu_job(job):
-    import numpy as np
+def run_reference_streams(seeds, nframes, cfg, keep_first=()):
+    """P = len(seeds) concurrent reference processes, one stream each (its own
+    keyframe window and d_pre chain over `nframes` frames). Returns per-seed
+    (frames, t0, t1, out_dir) in seed order; frames as ref.run_pipeline."""
+    import multiprocessing as mp
+    import shutil
+    import tempfile
 
-    from oracle import ref
-    from paper_2203_02300_b200.config import Config
+    ctx = mp.get_context("fork")
+    base = tempfile.mkdtemp(prefix="dco_refarm_")
+    barrier, q = ctx.Barrier(len(seeds)), ctx.Queue()
+    procs = []
+    for k, sd in enumerate(seeds):
+        job = (sd, nframes, os.path.join(base, "s%d" % sd), cfg.as_dict(), keep_first if k == 0 else ())
+        pr = ctx.Process(target=_ref_stream_worker, args=(job, barrier, q))
+        pr.start()
+        procs.append(pr)
+    got = {}
+    for _ in seeds:
+        sd, res, t0, t1, out = q.get()
+        got[sd] = (res, t0, t1, out)
+    for pr in procs:
+        pr.join()
+    bad = [str(v[0]) for v in got.values() if isinstance(v[0], str)]
+    if bad:
+        shutil.rmtree(base, ignore_errors=True)
+        raise RuntimeError(bad[0])
+    return [got[sd] for sd in seeds], base
 
-    (past8, mid8, fut8, right8), d_pre, cfg_dict = job
-    cfg = Config(**cfg_dict)
-    f = lambda a: a.astype(np.float32) / np.float32(255.0)  # noqa: E731  read_gray bytes/255.0f
-    mid = f(mid8)
-    q = [ref.downsample_half(f(a)) for a in (past8, mid8, fut8)]
-    rq = ref.downsample_half(f(right8))
-    vr, vd = _VIRT
-    out = ref.pipeline_frame(q[0], q[1], q[2], mid, rq, np.repeat(mid[:, :, None], 3, 2), d_pre, vr, vd, cfg)
-    return out["iterations"]
 
+def stage_table(frames_lists, reps_label):
+    """The reference's 14-stage schema (pipeline.cpp:57-82) over the given
+    frames: mean / min / max ms per stage and of the frame total."""
+    from paper_2203_02300_b200 import report
 
-_VIRT = (None, None)
+    samples = [f["stages"] for fl in frames_lists for f in fl]
+    totals = [f["total"] for fl in frames_lists for f in fl]
+    rows = report.summarize(samples, totals)
+    text = report.format_bench_report(len(samples), rows)
+    return {r[0]: round(r[1], 3) for r in rows}, "%s\n%s" % (reps_label, text)
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU implementation (oracle/_ref, built
-    from /root/reference sources) on the host cores, same config/metric."""
-    import numpy as np
+    """--impl reference: the reference's own frame loop dco::run_pipeline
+    (oracle/_ref, built unmodified from /root/reference) on every host core,
+    one stream per process, on this arm's config / metric. Each process runs
+    2 + 1 + W + K frames: the window fill, the first composited frame (no
+    d_pre), W warm-up and K timed steady frames; a step is one frame on every
+    process. value = sum over processes of K / (sum of its timed frames'
+    StageTimings totals)."""
+    import shutil
 
     from paper_2203_02300_b200.config import Config
-    from paper_2203_02300_b200.synth import StereoVideo
+    from paper_2203_02300_b200.sharding import stream_seeds
 
     if rank != 0:
         return
-    global _VIRT
-    from oracle import ref
-
     cfg = Config(d_max=D - 1)
-    vid = StereoVideo(W, H)
-    _VIRT = ref.render_cube(W, H, cfg.focal_px)
-    frames = []
-    for i in range(8):
-        l0, _ = vid.frame(i)
-        l1, r1 = vid.frame(i + 1)
-        l2, _ = vid.frame(i + 2)
-        frames.append((l0, l1, l2, r1))
-    # steady state needs a previous dense map: one reference frame provides it
-    f = lambda a: a.astype(np.float32) / np.float32(255.0)  # noqa: E731
-    q = [ref.downsample_half(f(a)) for a in frames[0][:3]]
-    out = ref.pipeline_frame(q[0], q[1], q[2], f(frames[0][1]), ref.downsample_half(f(frames[0][3])),
-                             np.repeat(f(frames[0][1])[:, :, None], 3, 2), None, _VIRT[0], _VIRT[1], cfg)
-    d_pre = [out["dense"]]
-    procs = cpu_procs()
-    times = []
-    for it in range(args.warmup + args.steps):
-        t = cpu_reference_frames(frames, d_pre, cfg.as_dict(), procs)
-        if it >= args.warmup:
-            times.append(t)
-    total = sum(times)
-    value = procs * len(times) / total
+    procs = min(cpu_procs(), 96)
+    nframes = 3 + args.warmup + args.steps
+    w0 = time.monotonic()
+    runs, base = run_reference_streams(stream_seeds(0, procs), nframes, cfg)
+    wall = time.monotonic() - w0
+    shutil.rmtree(base, ignore_errors=True)
+    timed = [res[1 + args.warmup: 1 + args.warmup + args.steps] for res, _, _, _ in runs]
+    if any(len(t) != args.steps for t in timed):
+        raise RuntimeError("reference run returned fewer composited frames than requested")
+    per_proc_s = [sum(f["total"] for f in t) / 1000.0 for t in timed]
+    value = sum(args.steps / s for s in per_proc_s)
+    ms_step = 1000.0 * statistics.mean(per_proc_s) / args.steps
+    iters = [f["iterations"] for t in timed for f in t]
+    stages, text = stage_table(timed, "reference run_pipeline, %d processes x %d timed frames" % (procs, args.steps))
+    print(text, file=sys.stderr)
+    sample = ("%d concurrent reference processes (dco::run_pipeline, oracle/_ref), one stream each: %d frames "
+              "(window fill + first frame + %d warm-up + %d timed steady frames); value from the reference's own "
+              "StageTimings frame totals; whole run %.1f s wall" % (procs, nframes, args.warmup, args.steps, wall))
     line = {
-        "metric": METRIC, "impl": "reference", "value": value, "unit": "frames/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / len(times),
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-        "config": {"workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+composite)",
-                   "frames_per_step": procs},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": "reference",
-                         "sample": "%d concurrent 1280x720 D=128 steady-state frames per step (oracle/_ref, "
-                                   "one process per core)" % procs},
+        "config": dict(CONFIG),
+        "arm": {"processes": procs, "cpu_model": cpu_model(), "frames_per_step": procs,
+                "densify_iterations_mean": statistics.mean(iters), "stage_ms": stages},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": "reference", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -289,7 +342,7 @@ def run_ours(args, world, rank, local):
     import torch
 
     torch.cuda.set_device(local)
-    from paper_2203_02300_b200 import dco
+    from paper_2203_02300_b200 import dco, report
     from paper_2203_02300_b200.config import Config
     from paper_2203_02300_b200.sharding import Group, stream_seeds
     from paper_2203_02300_b200.synth import StereoVideo
@@ -425,11 +478,10 @@ def run_ours(args, world, rank, local):
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-        "config": {"workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+composite)",
-                   "width": W, "height": H, "disparities": D, "streams_per_gpu": S, "frames_per_step": S * world,
-                   "l2": "flushed (160 MiB memset, L2 is 126 MB) before every frame, inside the timed region",
-                   "parallelism": "stream-sharded x%d, %d concurrent streams per GPU" % (world, S),
-                   "virtual_layer": "cube mesh rendered on the device per frame under a per-frame pose"},
+        "config": dict(CONFIG),
+        "arm": {"streams_per_gpu": S, "frames_per_step": S * world, "gpus": world,
+                "stage_ms_reference_schema": dict(zip(report.STAGE_NAMES,
+                                                      [round(x, 4) for x in report.stages_from_spans(spans, nt)]))},
         "roofline": roof,
         "aggregation_roofline": {"achieved": agg_ab / (per_frame["aggregate"] / 1000.0) / 1e9, "peak": peak,
                                  "unit": "GB/s", "frac": agg_ab / (per_frame["aggregate"] / 1000.0) / 1e9 / peak},
@@ -442,51 +494,88 @@ def run_ours(args, world, rank, local):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            line["cpu_baseline"] = cpu_baseline(streams[0], dev_l[0], dev_r[0], [f[0] for f in host[0]],
-                                                [f[1] for f in host[0]], cfg, pos[0], nframes)
-        except Exception as e:  # report, don't hide
-            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     for st in streams:
         st.close()
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        except Exception as e:  # report, don't hide
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:300]}
     print(json.dumps(line))
     group.close()
 
 
-def cpu_baseline(s, dev_l, dev_r, lefts, rights, cfg, i, nframes):
-    """The reference (oracle/_ref) timed on this box's host cores on a bounded
-    sample of the same workload: P concurrent steady-state frames."""
-    global _VIRT
+def cpu_baseline(cfg):
+    """The reference timed on this box's host cores on a bounded sample of the
+    same workload: P concurrent processes, each the reference's own
+    dco::run_pipeline over a 4-frame stream of the GPU arm's scene (window
+    fill, a first composited frame, then one timed steady frame, d_pre chained
+    by the reference itself). value = sum over processes of 1 / (its steady
+    frame's StageTimings total).
+
+    Parity on the same run: stream 0 (the GPU arm's stream-0 seed and poses)
+    is pushed through a fresh GPU stream; both composited frames' dense maps
+    (the reference's dense_NNNN.pfm) and CG iteration counts are compared."""
+    import shutil
+
     import numpy as np
     import torch
 
-    from oracle import ref
+    from oracle import refseq
+    from paper_2203_02300_b200 import dco
+    from paper_2203_02300_b200.sharding import stream_seeds
+    from paper_2203_02300_b200.synth import StereoVideo
 
-    # the fixed virtual layer the GPU arm composites against
-    vdepth = np.full((H, W), np.nan, np.float32)
-    vrgb = np.zeros((H, W, 3), np.float32)
-    vdepth[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = 1.5
-    vrgb[H // 3: 2 * H // 3, W // 3: 2 * W // 3] = (1.0, 0.55, 0.1)
-    _VIRT = (vrgb, vdepth)
-    procs = cpu_procs()
-    # previous dense of the frame before each sampled frame (from the GPU stream)
-    d_pre = torch.empty((H, W), dtype=torch.float32, device="cuda")
-    frames, pres = [], []
-    for k in range(procs):
-        s.push_gray8(dev_l[i % nframes], dev_r[i % nframes], want_result=False)
-        v = s.views()
-        from paper_2203_02300_b200 import dco
+    procs = min(cpu_procs(), 96)
+    seeds = stream_seeds(0, procs)
+    nframes = 4
+    w0 = time.monotonic()
+    runs, base = run_reference_streams(seeds, nframes, cfg, keep_first=(1, 2))
+    wall = time.monotonic() - w0
+    steady = [res[1] for res, _, _, _ in runs]
+    value = sum(1000.0 / f["total"] for f in steady)
+    stages, text = stage_table([[f] for f in steady], "cpu_baseline: reference run_pipeline, steady frame x %d" % procs)
+    print(text, file=sys.stderr)
 
-        d_pre.copy_(dco.view_tensor(v.dense, (H, W), torch.float32))
-        pres.append(d_pre.cpu().numpy())
-        frames.append((lefts[(i - 1) % nframes], lefts[i % nframes], lefts[(i + 1) % nframes], rights[i % nframes]))
-        i += 1
-    ref.lib()
-    wall = cpu_reference_frames(frames, pres, cfg.as_dict(), procs)
-    return {"value": procs / wall, "unit": "frames/s", "cores": procs, "kind": "reference",
-            "sample": "%d concurrent 1280x720 D=128 steady-state frames (reference library oracle/_ref, "
-                      "one process per core), wall %.1f s" % (procs, wall)}
+    # GPU vs reference on stream 0
+    res0, _, _, out0 = runs[0]
+    vid = StereoVideo(W, H, seed=seeds[0])
+    s = dco.Stream(W, H, cfg)
+    v, t, c = cube_mesh(0.3)
+    s.set_mesh(v, t, c)
+    gpu_iters, max_abs = [], []
+    for i in range(nframes):
+        l8, r8 = vid.frame(i)
+        s.set_next_pose(frame_pose(i))
+        r = s.push_gray8(torch.from_numpy(l8).cuda(), torch.from_numpy(r8).cuda())
+        if r.composited:
+            torch.cuda.synchronize()
+            dense = dco.view_tensor(s.views().dense, (H, W), torch.float32).cpu().numpy()
+            want = refseq.read_pfm(os.path.join(out0, "dense_%04d.pfm" % (i - 1)))
+            want = np.where(np.isinf(want), np.nan, want)
+            gpu_iters.append(int(r.densify_iterations))
+            max_abs.append(float(np.nanmax(np.abs(dense.astype(np.float64) - want))))
+    s.close()
+    shutil.rmtree(base, ignore_errors=True)
+    return {"value": value, "unit": "frames/s", "cores": procs, "kind": "reference", "cpu_model": cpu_model(),
+            "sample": "%d concurrent reference processes (dco::run_pipeline, oracle/_ref), one 4-frame stream each; "
+                      "timed: each stream's steady frame (StageTimings total); run wall %.1f s" % (procs, wall),
+            "stage_ms": stages,
+            "parity_stream0": {"reference_iterations": [f["iterations"] for f in res0],
+                               "gpu_iterations": gpu_iters, "dense_max_abs_m": max_abs,
+                               "frames": "first composited (no d_pre) and steady"}}
+
+
+def relaunch_under_torchrun(n):
+    """`python bench.py --gpus N` without torchrun: re-exec with N ranks."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % n,
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -500,7 +589,16 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch_under_torchrun(args.gpus)
     world, rank, local = dist_setup()
+    if world != args.gpus:
+        sys.exit("bench.py: --gpus %d but WORLD_SIZE=%d (launch one rank per GPU)" % (args.gpus, world))
+    if args.impl == "ours":
+        import torch
+
+        if torch.cuda.device_count() < world:
+            sys.exit("bench.py: --gpus %d but only %d visible GPUs" % (world, torch.cuda.device_count()))
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

@@ -101,6 +101,9 @@ int dco_set_stream(dco_ctx* ctx, void* stream);
 int dco_synchronize(dco_ctx* ctx);
 /* Number of kernels this context has launched (for the bench's launch count). */
 uint64_t dco_kernel_launches(const dco_ctx* ctx);
+/* Kernel instance that ran this context's last dense solve, e.g.
+ * "k_pcg_tmem<7>" (tests pin the headline instance; "" before any solve). */
+const char* dco_last_solver(const dco_ctx* ctx);
 
 /* ---- config (config.hpp:11-60, config.cpp:10-36) ----------------------- */
 void dco_config_default(dco_config* cfg);

@@ -64,6 +64,9 @@ def lib():
             "ref_render_cube": (I, [ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, D, I, I, P, P]),
             "ref_render_virtual": (I, [P, I, P, I, P, P, D, D, D, I, I, P, P]),
             "ref_transform_mesh": (I, [P, I, P, P]),
+            "ref_run_pipeline": (I, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, I, P, P, P,
+                                     ctypes.POINTER(I)]),
+            "ref_format_bench_report": (I, [I, P, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p]),
             "ref_pipeline_frame": (I, [I, I, P, P, P, P, P, P, P, P, P, CFG, P, P, P, P, P, ctypes.POINTER(I),
                                        ctypes.POINTER(D)]),
         }
@@ -374,6 +377,36 @@ def pipeline_frame(past_q, mid_q, future_q, mid_gray, right_q, mid_rgb, d_pre, v
         _check(st)
     return {"dense": dense, "composite": comp, "mask": mask, "edges": edges, "sparse": sparse,
             "iterations": it.value, "objective": obj.value, "unsolvable": st == 3}
+
+
+STAGES = ["adaptive filter area construction", "initial parallax", "parallax optimisation", "sparse map",
+          "bidirectional optical flow", "amplitude", "fusion", "box filter", "normalisation", "Gaussian filtering",
+          "depth contour extraction", "densification", "rendering", "other"]
+
+
+def run_pipeline(config_path, manifest, out_dir, mesh_path=None, cap=4096):
+    """run_pipeline (pipeline.cpp:108-321), the reference's own frame loop over
+    a manifest. -> list of dicts per composited frame: index, iterations,
+    stages (the 14 StageTimings values, StageTimings::stage_names order) and
+    total (ms, the reference's own steady_clock timers)."""
+    ms = np.zeros((cap, 15), np.float64)
+    it = np.zeros(cap, np.int32)
+    idx = np.zeros(cap, np.int32)
+    n = ctypes.c_int(0)
+    _check(lib().ref_run_pipeline(config_path.encode() if config_path else None, manifest.encode(), out_dir.encode(),
+                                  mesh_path.encode() if mesh_path else None, cap, _p(ms), _p(it), _p(idx),
+                                  ctypes.byref(n)))
+    return [{"index": int(idx[k]), "iterations": int(it[k]), "stages": ms[k, :14].tolist(), "total": float(ms[k, 14])}
+            for k in range(n.value)]
+
+
+def format_bench_report(repetitions, mmm, csv_path=None):
+    """format_bench_report (+ write_bench_csv when csv_path), pipeline.cpp:366-391,
+    of 15 (mean, min, max) rows: the 14 stages then the frame total."""
+    a = _c(mmm, np.float64)
+    buf = ctypes.create_string_buffer(8192)
+    _check(lib().ref_format_bench_report(repetitions, _p(a), buf, 8192, csv_path.encode() if csv_path else None))
+    return buf.value.decode()
 
 
 def lr_consistency(disp_left, disp_right, max_diff=1.0):

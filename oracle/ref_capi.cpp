@@ -19,6 +19,7 @@
 #include "dco/error.hpp"
 #include "dco/flow.hpp"
 #include "dco/occlude.hpp"
+#include "dco/pipeline.hpp"
 #include "dco/pyramid.hpp"
 #include "dco/stereo.hpp"
 #include "dco/synth.hpp"
@@ -662,6 +663,54 @@ int ref_pipeline_frame(int fw, int fh, const float* past_q, const float* mid_q,
         if (edges_out) copy_out(cont.edges.data, edges_out);
         if (sparse_out) copy_out(sparse.data, sparse_out);
         if (unsolvable) throw UnsolvableFrameError("solve_dense_depth: no anchored pixel");
+    });
+}
+
+// run_pipeline (pipeline.cpp:108-321), the reference's own public frame loop:
+// config file, manifest of PGM frames with per-frame poses, OBJ mesh, outputs
+// under out_dir. Per composited frame (in index order, at most cap): the 14
+// StageTimings values + the frame total (15 doubles, pipeline.cpp:57-82) into
+// stage_ms, the CG iteration count into iterations and the frame index into
+// index. *n = number of composited frames.
+int ref_run_pipeline(const char* config_path, const char* manifest, const char* out_dir, const char* mesh_path,
+                     int cap, double* stage_ms, int* iterations, int* index, int* n) {
+    return guarded([&] {
+        RunOptions o;
+        o.config_path = config_path ? config_path : "";
+        o.manifest_path = manifest;
+        o.output_dir = out_dir;
+        o.mesh_path = mesh_path ? mesh_path : "";
+        RunSummary sum = run_pipeline(o);
+        int k = 0;
+        for (const FrameResult& f : sum.frames) {
+            if (!f.composited || k >= cap) continue;
+            std::vector<double> v = f.timings.stage_values();
+            for (size_t i = 0; i < v.size(); ++i) stage_ms[15 * k + i] = v[i];
+            stage_ms[15 * k + 14] = f.timings.total;
+            iterations[k] = f.densify_iterations;
+            index[k] = f.index;
+            ++k;
+        }
+        *n = k;
+    });
+}
+
+// format_bench_report / write_bench_csv (pipeline.cpp:366-391) of a report
+// whose 14 rows carry the StageTimings::stage_names() (pipeline.cpp:57-75) and
+// whose total is "frame processing"; mmm = 15 x (mean, min, max). The text goes
+// to out (NUL-terminated, truncated to cap); csv_path may be NULL.
+int ref_format_bench_report(int repetitions, const double* mmm, char* out, size_t cap, const char* csv_path) {
+    return guarded([&] {
+        BenchReport r;
+        r.repetitions = repetitions;
+        const auto& names = StageTimings::stage_names();
+        for (size_t i = 0; i < names.size(); ++i)
+            r.rows.push_back({names[i], mmm[3 * i], mmm[3 * i + 1], mmm[3 * i + 2]});
+        r.total = {"frame processing", mmm[3 * 14], mmm[3 * 14 + 1], mmm[3 * 14 + 2]};
+        std::string text = format_bench_report(r);
+        std::strncpy(out, text.c_str(), cap - 1);
+        out[cap - 1] = 0;
+        if (csv_path) write_bench_csv(r, csv_path);
     });
 }
 

@@ -91,12 +91,25 @@ struct dco_ctx {
     dco_gpu::DevBuf slots[dco_gpu::S_COUNT];
     void* pinned = nullptr;  // small pinned host staging area for scalar readbacks
     size_t pinned_bytes = 0;
+    const char* last_solver = "";  // kernel instance of the last dense solve
 };
 
 namespace dco_gpu {
 
 void* scratch(dco_ctx* ctx, Slot s, size_t bytes);
 void* pinned_host(dco_ctx* ctx, size_t bytes);
+
+// Raises fn's dynamic shared-memory cap to `bytes` (and the shared-memory
+// carveout to 100 % when `carveout`) on the context's device, once per
+// (device, kernel, size): function attributes are per device, so a process
+// holding contexts on several GPUs sets them on each.
+void smem_attr(dco_ctx* ctx, const void* fn, int bytes, bool carveout = false);
+template <typename K>
+inline void smem_attr(dco_ctx* ctx, K* fn, int bytes, bool carveout = false) {
+    smem_attr(ctx, reinterpret_cast<const void*>(fn), bytes, carveout);
+}
+// Multiprocessor count of the context's device (cached per device).
+int sm_count(dco_ctx* ctx);
 
 // Counts and error-checks every launch made through it.
 inline void launched(dco_ctx* ctx, const char* name) {
@@ -114,6 +127,9 @@ template <typename F>
 int guarded(dco_ctx* ctx, F&& fn) {
     try {
         if (!ctx) return DCO_INPUT;
+        // every entry point runs on the context's device, whatever the
+        // calling thread's current device is
+        cuda_check(cudaSetDevice(ctx->device), "set device");
         fn();
         return DCO_OK;
     } catch (const Failure& f) {

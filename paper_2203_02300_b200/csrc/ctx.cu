@@ -4,6 +4,9 @@
 #include <math.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace dco_gpu {
@@ -71,6 +74,30 @@ void make_stereo_tables(const dco_config* cfg, StereoTables* t) {
         t->census[h] = 1.0 - exp(-static_cast<double>(h) / cfg->lambda_census);
 }
 
+void smem_attr(dco_ctx* ctx, const void* fn, int bytes, bool carveout) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    int& have = done[{ctx->device, fn}];
+    if (have >= bytes) return;
+    cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attr");
+    if (carveout)
+        cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+    have = bytes;
+}
+
+int sm_count(dco_ctx* ctx) {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(ctx->device);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, ctx->device), "sm count");
+    cache[ctx->device] = n;
+    return n;
+}
+
 }  // namespace dco_gpu
 
 using namespace dco_gpu;
@@ -116,6 +143,8 @@ int dco_synchronize(dco_ctx* ctx) {
 }
 
 uint64_t dco_kernel_launches(const dco_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* dco_last_solver(const dco_ctx* ctx) { return ctx ? ctx->last_solver : ""; }
 
 void dco_config_default(dco_config* c) {
     if (!c) return;

@@ -19,6 +19,8 @@
 #include <math.h>
 
 #include <mutex>
+#include <set>
+#include <string>
 
 #include "common.cuh"
 #include "grid_reduce.cuh"
@@ -693,7 +695,14 @@ inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + 
 
 long long* g_pcg_dbg = nullptr;
 constexpr int kDbgLen = 1280 + 64 * 1024 * 3;  // + per-block globaltimer stamps
-int g_sms = 0;
+
+// "k_pcg_tmem<7>"-style instance names with stable storage (dco_last_solver)
+const char* instance_name(const char* base, int ept) {
+    static std::mutex mu;
+    static std::set<std::string> names;
+    std::lock_guard<std::mutex> lock(mu);
+    return names.insert(std::string(base) + "<" + std::to_string(ept) + ">").first->c_str();
+}
 
 typedef void (*OnchipKernel)(CGArgs, int, GridBar*);
 constexpr int kOnchipThreadsUsed = 1024;
@@ -879,7 +888,10 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     }
     // on-chip resident path: one 1024-thread block per SM, chunk of unknowns
     // per block with 4 doubles each in shared memory, <= 8 per thread
-    const int sms = g_sms ? g_sms : (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, ctx->device), g_sms);
+    // DCO_PCG_BLOCKS=k (tests): a k-block grid instead of one block per SM, so
+    // a small system reaches the per-thread slot counts (EPT) of a large one
+    int sms = sm_count(ctx);
+    if (const char* fb = getenv("DCO_PCG_BLOCKS")) sms = std::max(1, std::min(sms, atoi(fb)));
     const int chunk = static_cast<int>((n + sms - 1) / sms);
     const int threads = kOnchipThreadsUsed;
     const int ept = (chunk + threads - 1) / threads;
@@ -898,13 +910,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         const size_t smem_s = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
         BigKernel sk = share_for(ept_s);
         if (sk && smem_s <= kOnchipSmemMax) {
-            static int attr_s[17] = {};
-            if (attr_s[ept_s] < static_cast<int>(smem_s)) {
-                cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(sk),
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_s)),
-                           "smem attr");
-                attr_s[ept_s] = static_cast<int>(smem_s);
-            }
+            smem_attr(ctx, sk, static_cast<int>(smem_s));
             int chunk_arg = chunk;
             GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
             cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
@@ -913,19 +919,14 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
             launch_cooperative_serialized(ctx, reinterpret_cast<void*>(sk), dim3(sms), dim3(kShareThreads), params,
                                           smem_s);
             launched(ctx, "k_pcg_share");
+            ctx->last_solver = instance_name("k_pcg_share", ept_s);
             return;
         }
     }
     if (kern && !force_big && smem <= kOnchipSmemMax && sms <= 1024) {
         // dynamic shared memory: exactly this launch's need (static scratch
         // comes on top, 227 KB per CTA in total)
-        static int attr[2][17] = {};
-        if (attr[no_tmem][ept] < static_cast<int>(smem)) {
-            cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-                       "smem attr");
-            attr[no_tmem][ept] = static_cast<int>(smem);
-        }
+        smem_attr(ctx, kern, static_cast<int>(smem));
         int chunk_arg = chunk;
         GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
         cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
@@ -933,6 +934,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(threads),
                                       params, smem);
         launched(ctx, no_tmem ? "k_pcg_onchip" : "k_pcg_tmem");
+        ctx->last_solver = instance_name(no_tmem ? "k_pcg_onchip" : "k_pcg_tmem", ept);
         return;
     }
     // larger frames: p on chip, q/rs in TMEM, r in registers, the rest L2-resident
@@ -941,14 +943,8 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         const size_t smem_b = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
         BigKernel bk = big_for(ept_b < 9 ? 9 : ept_b);
         if (bk && !force_stream && smem_b <= kOnchipSmemMax && sms <= 1024 && !getenv("DCO_PCG_NO_BIG")) {
-            static int attr_b[22] = {};
             const int e = ept_b < 9 ? 9 : ept_b;
-            if (attr_b[e] < static_cast<int>(smem_b)) {
-                cuda_check(cudaFuncSetAttribute(reinterpret_cast<const void*>(bk),
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_b)),
-                           "smem attr");
-                attr_b[e] = static_cast<int>(smem_b);
-            }
+            smem_attr(ctx, bk, static_cast<int>(smem_b));
             int chunk_arg = chunk;
             GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
             cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
@@ -957,6 +953,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
             launch_cooperative_serialized(ctx, reinterpret_cast<void*>(bk), dim3(sms), dim3(kBigThreads), params,
                                           smem_b);
             launched(ctx, "k_pcg_big");
+            ctx->last_solver = instance_name("k_pcg_big", e);
             return;
         }
     }
@@ -981,6 +978,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         const int threads = 512;
         launch_cooperative_serialized(ctx, fn, dim3(sms), dim3(threads), params, 0);
         launched(ctx, "k_pcg_stream");
+        ctx->last_solver = "k_pcg_stream<512,2>";
     }
 }
 
@@ -1361,7 +1359,7 @@ void band_fill(dco_band_solver* s, const dco_system* sys, const dco_config* cfg,
 }
 
 void band_launch(dco_ctx* ctx, dco_band_solver* const* ss, int count) {
-    const int sms = g_sms ? g_sms : (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, ctx->device), g_sms);
+    const int sms = sm_count(ctx);
     const int bpr = std::min<int>(static_cast<int>(kBandMaxBlocks), sms / count);
     require(bpr >= 1, "band solver: more ranks on this GPU than SMs");
     BandRank* dd = ss[0]->desc_dev;

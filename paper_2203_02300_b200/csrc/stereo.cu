@@ -1600,12 +1600,7 @@ void aggregate_band_hpass(dco_ctx* ctx, const float* cost, int w, int h, int nd,
     const int ring_h = 2 * max_arm + 2 + kBandHPF - 1;
     dim3 tb(32, 4);
     const size_t smem_h = static_cast<size_t>(ring_h) * kAggThreads * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_agg_h2<kBandHPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_agg_h2<kBandHPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
-    }
+    smem_attr(ctx, k_agg_h2<kBandHPF>, 227 * 1024, true);
     k_agg_h2<kBandHPF><<<dim3((nd + 31) / 32, (h + 3) / 4), tb, smem_h, ctx->stream>>>(cost, w, h, nd, hinfo, lag,
                                                                                       ring_h, hsum);
     launched(ctx, "k_agg_h2");
@@ -1621,12 +1616,7 @@ void aggregate_band_vpass(dco_ctx* ctx, int w, int h, int nd, int max_arm, float
     const int ring_v = 2 * max_arm + 2 + kBandVPF - 1;
     dim3 tb(32, 4);
     const size_t smem_v = static_cast<size_t>(ring_v) * kAggThreads * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_agg_v2<kBandVPF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_agg_v2<kBandVPF, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
-    }
+    smem_attr(ctx, k_agg_v2<kBandVPF, true>, 227 * 1024, true);
     k_agg_v2<kBandVPF, true><<<dim3((k1 - k0 + 31) / 32, (w + 3) / 4), tb, smem_v, ctx->stream>>>(
         hsum, w, h, nd, vinfo, lag, ring_v, out, carry_in, c0, carry_out, e, k0, k1);
     launched(ctx, "k_agg_v2_band");
@@ -1653,14 +1643,8 @@ void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, cons
         dim3 tb(32, 4);
         const size_t smem_h = static_cast<size_t>(ring_h) * kAggThreads * sizeof(double);
         const size_t smem_v = static_cast<size_t>(ring_v) * kAggThreads * sizeof(double);
-        static bool attr2 = false;
-        if (!attr2) {
-            cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            cudaFuncSetAttribute(k_agg_v2<kVPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            cudaFuncSetAttribute(k_agg_h2<kHPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            cudaFuncSetAttribute(k_agg_v2<kVPF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            attr2 = true;
-        }
+        smem_attr(ctx, k_agg_h2<kHPF>, 227 * 1024, true);
+        smem_attr(ctx, k_agg_v2<kVPF>, 227 * 1024, true);
         k_agg_h2<kHPF><<<dim3((nd + 31) / 32, (h + 3) / 4), tb, smem_h, ctx->stream>>>(cost, w, h, nd, hinfo, lag,
                                                                                       ring_h, hsum);
         launched(ctx, "k_agg_h2");
@@ -1677,12 +1661,8 @@ void aggregate_costs(dco_ctx* ctx, const float* cost, int w, int h, int nd, cons
     while (rows > 1 && static_cast<size_t>(ring) * 32 * rows * sizeof(double) > 200 * 1024) rows >>= 1;
     dim3 tb(32, rows);
     size_t smem = static_cast<size_t>(ring) * 32 * rows * sizeof(double);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_agg_hpass, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_agg_vpass, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_set = true;
-    }
+    smem_attr(ctx, k_agg_hpass, 227 * 1024);
+    smem_attr(ctx, k_agg_vpass, 227 * 1024);
     dim3 gh((nd + 31) / 32, (h + rows - 1) / rows);
     k_agg_hpass<<<gh, tb, smem, ctx->stream>>>(cost, w, h, nd, l, r, lag, ring - 1, hsum);
     launched(ctx, "k_agg_hpass");
@@ -1724,11 +1704,7 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     const int warps = 8;
     const int rows_cap = 2 * max_arm + 2;
     size_t smem = static_cast<size_t>(warps) * (cap + 3 * rows_cap + 1) * sizeof(unsigned);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_hist_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_set = true;
-    }
+    smem_attr(ctx, k_hist_refine, 227 * 1024);
     float* bufs[2] = {static_cast<float*>(scratch(ctx, S_DISP0, n * 4)),
                       static_cast<float*>(scratch(ctx, S_DISP1, n * 4))};
     const float* src = disp;
@@ -1740,17 +1716,13 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     const int vwarps = 4;
     const size_t vsmem = static_cast<size_t>(vwarps) * ring * nbp * sizeof(unsigned short);
     const size_t hsmem = static_cast<size_t>(nbp) * ((w + 31) / 32) * sizeof(unsigned);
-    static bool attr_v = false;
-    if (!attr_v) {
-        cudaFuncSetAttribute(k_refine_vmode3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode3<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(k_refine_vmode2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_v = true;
-    }
+    smem_attr(ctx, k_refine_vmode3<2>, 227 * 1024);
+    smem_attr(ctx, k_refine_vmode3<4>, 227 * 1024);
+    smem_attr(ctx, k_refine_vmode3<8>, 227 * 1024);
+    smem_attr(ctx, k_refine_vmode2<1>, 227 * 1024);
+    smem_attr(ctx, k_refine_vmode2<2>, 227 * 1024);
+    smem_attr(ctx, k_refine_vmode2<4>, 227 * 1024);
+    smem_attr(ctx, k_refine_vmode2<8>, 227 * 1024);
     const bool aggregated = nbp && vsmem <= 200 * 1024 && hsmem <= 200 * 1024;
     // packed u16 pairs: every column prefix stays below 65536
     const bool packed = aggregated && nbp >= 64 && static_cast<long>(h) * (2 * max_arm + 1) < 65536;
@@ -1758,11 +1730,7 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     const size_t vsmem3 = static_cast<size_t>(vwarps) * ring3 * 32 * (nbp / 64) * sizeof(uint32_t);
     const bool per_thread = cap <= 256;
     const size_t smem_t = static_cast<size_t>(cap) * kHistThreads * sizeof(unsigned short);
-    static bool attr_t = false;
-    if (per_thread && !attr_t) {
-        cudaFuncSetAttribute(k_hist_refine_thread, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_t = true;
-    }
+    smem_attr(ctx, k_hist_refine_thread, 227 * 1024);
     const unsigned blocks_t = static_cast<unsigned>(std::min<size_t>(blocks_for(n, kHistThreads), 148 * 8));
     for (int it = 0; it < iters; ++it) {
         float* dst = (it == iters - 1) ? out : bufs[it & 1];

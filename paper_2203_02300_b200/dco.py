@@ -52,6 +52,11 @@ def kernel_launches(device=None):
     return native.load().dco_kernel_launches(context(device))
 
 
+def last_solver(ctx=None):
+    """Kernel instance of the context's last dense solve, e.g. "k_pcg_tmem<7>"."""
+    return native.load().dco_last_solver(context() if ctx is None else ctx).decode()
+
+
 def _p(t):
     if t is None:
         return None
@@ -748,6 +753,9 @@ class Stream:
 
     def launches(self):
         return self.lib.dco_kernel_launches(self.ctx)
+
+    def last_solver(self):
+        return last_solver(self.ctx)
 
     def set_virtual(self, virt_rgb, virt_depth):
         self._bind()

@@ -100,6 +100,7 @@ SIGNATURES = {
     "dco_set_stream": (c_int, [c_void_p, c_void_p]),
     "dco_synchronize": (c_int, [c_void_p]),
     "dco_kernel_launches": (c_uint64, [c_void_p]),
+    "dco_last_solver": (c_char_p, [c_void_p]),
     "dco_config_default": (None, [CFG]),
     "dco_config_validate": (c_int, [CFG, c_char_p, c_size_t]),
     "dco_downsample_half": (c_int, [c_void_p, P, c_int, c_int, P]),

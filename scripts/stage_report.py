@@ -7,19 +7,7 @@ line by line.
   python scripts/stage_report.py [--width 1280 --height 720 --disparities 128
                                   --frames 8 --repetitions 3 --csv out.csv]
 
-Stage mapping (the stream's CUDA-event spans, one stream alone):
-  adaptive filter area construction <- cross
-  initial parallax                  <- cost + aggregate + wta
-  parallax optimisation             <- refine
-  sparse map                        <- sparse
-  bidirectional optical flow        <- flow
-  amplitude + fusion                <- fusion (one fused kernel; reported under
-                                       "fusion", "amplitude" = 0)
-  box filter, normalisation, Gaussian filtering, depth contour extraction
-                                    <- box, normalize, blur, contour
-  densification                     <- assemble + solve
-  rendering                         <- composite (includes the virtual layer)
-  other                             <- ingest (u8 decode + downsample)
+Stage mapping (CUDA-event spans -> the 14 stages): paper_2203_02300_b200/report.py.
 """
 import argparse
 import os
@@ -30,24 +18,8 @@ import torch  # noqa: E402
 
 from paper_2203_02300_b200 import dco  # noqa: E402
 from paper_2203_02300_b200.config import Config  # noqa: E402
+from paper_2203_02300_b200.report import bench_csv, format_bench_report, stages_from_spans, summarize  # noqa: E402
 from paper_2203_02300_b200.synth import StereoVideo  # noqa: E402
-
-STAGES = [
-    ("adaptive filter area construction", ["cross"]),
-    ("initial parallax", ["cost", "aggregate", "wta"]),
-    ("parallax optimisation", ["refine"]),
-    ("sparse map", ["sparse"]),
-    ("bidirectional optical flow", ["flow"]),
-    ("amplitude", []),
-    ("fusion", ["fusion"]),
-    ("box filter", ["box"]),
-    ("normalisation", ["normalize"]),
-    ("Gaussian filtering", ["blur"]),
-    ("depth contour extraction", ["contour"]),
-    ("densification", ["assemble", "solve"]),
-    ("rendering", ["composite"]),
-    ("other", ["ingest"]),
-]
 
 
 def run_once(W, H, cfg, frames):
@@ -58,8 +30,7 @@ def run_once(W, H, cfg, frames):
         s.push_gray8(l8, r8, want_result=False)
     spans, n = s.span_times()
     s.close()
-    per = {name: sum(spans[k] for k in keys) / max(n, 1) for name, keys in STAGES}
-    return per, sum(spans.values()) / max(n, 1)
+    return stages_from_spans(spans, n), sum(spans.values()) / max(n, 1)
 
 
 def main():
@@ -78,24 +49,16 @@ def main():
     vid = StereoVideo(W, H)
     frames = [tuple(torch.from_numpy(x).cuda() for x in vid.frame(i)) for i in range(a.frames)]
     run_once(W, H, cfg, frames)  # warm-up, excluded from statistics (pipeline.cpp:327)
-    samples = {name: [] for name, _ in STAGES}
-    totals = []
+    samples, totals = [], []
     for _ in range(a.repetitions):
         per, total = run_once(W, H, cfg, frames)
-        for k, v in per.items():
-            samples[k].append(v)
+        samples.append(per)
         totals.append(total)
-    rows = [(name, sum(v) / len(v), min(v), max(v)) for name, v in samples.items()]
-    rows.append(("frame processing", sum(totals) / len(totals), min(totals), max(totals)))
-    print("repetitions: %d" % a.repetitions)
-    print("%-36s %10s %10s %10s" % ("stage", "mean(ms)", "min(ms)", "max(ms)"))
-    for r in rows:
-        print("%-36s %10.2f %10.2f %10.2f" % r)
+    rows = summarize(samples, totals)
+    print(format_bench_report(a.repetitions, rows), end="")
     if a.csv:
         with open(a.csv, "w") as f:
-            f.write("stage,mean_ms,min_ms,max_ms\n")
-            for r in rows:
-                f.write("%s,%g,%g,%g\n" % r)
+            f.write(bench_csv(rows))
 
 
 if __name__ == "__main__":
