@@ -78,6 +78,9 @@ enum Slot : int {
     S_RENDER_LIST,
     S_HIST,
     S_STAGE,
+    S_FIXLIST,
+    S_BADROW,
+    S_EXPORT,
     S_COUNT
 };
 

@@ -32,9 +32,9 @@ void render_virtual(dco_ctx* ctx, const float* verts, const int* tris, const flo
 bool stereo_slices_supported(int max_arm);
 void cost_volume_slices(dco_ctx* ctx, const float* left, const float* right, int w, int h, const uint8_t* l,
                         const uint8_t* r, const uint8_t* u, const uint8_t* d, const dco_config* cfg, int max_arm,
-                        float* cost, int* unsafe);
+                        float* cost, int* rect);
 void aggregate_slices(dco_ctx* ctx, const float* cost, int w, int h, int nd, const uint8_t* l, const uint8_t* r,
-                      const uint8_t* u, const uint8_t* d, int max_arm, const int* unsafe, float* agg);
+                      const uint8_t* u, const uint8_t* d, int max_arm, const int* rect, float* agg);
 void wta_slices(dco_ctx* ctx, const float* agg, int w, int h, int d_min, int nd, float* disp);
 void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, const uint8_t* l,
                                 const uint8_t* r, const uint8_t* u, const uint8_t* d, int iters, int bin_bound,
@@ -251,9 +251,9 @@ void stereo_chain(dco_stream* s, const float* lq, const float* rq, float* out) {
     uint8_t *L = s->arms, *R = L + nq, *U = R + nq, *D = U + nq;
     build_cross_windows(ctx, lq, qw, qh, cfg, L, R, U, D);
     if (stereo_slices_supported(cfg->cross_arm_l1)) {
-        int* unsafe = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, static_cast<size_t>(s->nd) * sizeof(int)));
-        cost_volume_slices(ctx, lq, rq, qw, qh, L, R, U, D, cfg, cfg->cross_arm_l1, s->cost, unsafe);
-        aggregate_slices(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, unsafe, s->agg);
+        int* rect = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, 2 * static_cast<size_t>(s->nd) * sizeof(int)));
+        cost_volume_slices(ctx, lq, rq, qw, qh, L, R, U, D, cfg, cfg->cross_arm_l1, s->cost, rect);
+        aggregate_slices(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, rect, s->agg);
         wta_slices(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
     } else {
         compute_cost_volume(ctx, lq, rq, qw, qh, L, R, U, D, cfg, s->cost);
@@ -282,11 +282,11 @@ void run_frame(dco_stream* s, dco_frame_result* res) {
     s->mark(DCO_SPAN_CROSS + 1);
     if (stereo_slices_supported(cfg->cross_arm_l1)) {
         // slice-major cost volume + exact fixed-point aggregation (stereo_slices.cu)
-        int* unsafe = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, static_cast<size_t>(s->nd) * sizeof(int)));
+        int* rect = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, 2 * static_cast<size_t>(s->nd) * sizeof(int)));
         cost_volume_slices(ctx, s->left_q[mid], s->right_q[mid], qw, qh, L, R, U, D, cfg, cfg->cross_arm_l1, s->cost,
-                           unsafe);
+                           rect);
         s->mark(DCO_SPAN_COST + 1);
-        aggregate_slices(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, unsafe, s->agg);
+        aggregate_slices(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, rect, s->agg);
         s->mark(DCO_SPAN_AGGREGATE + 1);
         wta_slices(ctx, s->agg, qw, qh, cfg->d_min, s->nd, s->disp_wta);
     } else {
@@ -738,9 +738,9 @@ int dco_stereo_sparse_depth(dco_ctx* ctx, const float* left_q, const float* righ
         uint8_t *L = arms, *R = arms + nq, *U = arms + 2 * nq, *D = arms + 3 * nq;
         build_cross_windows(ctx, left_q, w, h, cfg, L, R, U, D);
         if (stereo_slices_supported(cfg->cross_arm_l1)) {
-            int* unsafe = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, static_cast<size_t>(nd) * sizeof(int)));
-            cost_volume_slices(ctx, left_q, right_q, w, h, L, R, U, D, cfg, cfg->cross_arm_l1, cost, unsafe);
-            aggregate_slices(ctx, cost, w, h, nd, L, R, U, D, cfg->cross_arm_l1, unsafe, agg);
+            int* rect = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, 2 * static_cast<size_t>(nd) * sizeof(int)));
+            cost_volume_slices(ctx, left_q, right_q, w, h, L, R, U, D, cfg, cfg->cross_arm_l1, cost, rect);
+            aggregate_slices(ctx, cost, w, h, nd, L, R, U, D, cfg->cross_arm_l1, rect, agg);
             wta_slices(ctx, agg, w, h, cfg->d_min, nd, d0);
         } else {
             compute_cost_volume(ctx, left_q, right_q, w, h, L, R, U, D, cfg, cost);
