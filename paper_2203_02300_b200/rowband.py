@@ -50,6 +50,10 @@ class LocalLinks:
     def gather_bytes(self, blobs):
         return [blobs[k] for k in range(self.bands)]
 
+    def gather_rows(self, rows):
+        """Every band's rows, stacked in band (= row) order."""
+        return torch.cat([rows[k] for k in range(self.bands)], dim=0)
+
 
 class DistLinks:
     """One band per rank over torch.distributed (rank k owns band k)."""
@@ -79,6 +83,18 @@ class DistLinks:
         out = [None] * self.bands
         self.dist.all_gather_object(out, blobs[self.rank])
         return out
+
+    def gather_rows(self, rows):
+        """Every rank's band rows, stacked in band order (bands differ in
+        height: padded to the tallest for the all_gather, then trimmed)."""
+        mine = rows[self.rank]
+        heights = self.gather_stats({self.rank: [float(mine.shape[0]), 0.0, 0.0, 0.0]})
+        hmax = int(max(h[0] for h in heights))
+        pad = torch.zeros((hmax,) + tuple(mine.shape[1:]), dtype=mine.dtype, device=mine.device)
+        pad[: mine.shape[0]] = mine
+        out = [torch.empty_like(pad) for _ in range(self.bands)]
+        self.dist.all_gather(out, pad)
+        return torch.cat([o[: int(h[0])] for o, h in zip(out, heights)], dim=0)
 
 
 class RowBandFrames:
@@ -126,6 +142,8 @@ class RowBandFrames:
             s.close()
         self.solvers = {}
 
+    force_sequential_mean = False  # tests: take the gathered sequential mean even inside the guard
+
     def _sub(self, b):
         """Full rows of a band's assembly sub-frame: owned + 2 (even start)."""
         return max(0, b.frow0 - 2), min(self.fh, b.frow1 + 2)
@@ -170,8 +188,11 @@ class RowBandFrames:
         stats = {k: self._sparse_stats(sparse[k]) for k in self.plans}
         allstats = L.gather_stats(stats)
         mean, exact = self._combine(allstats)
-        if not exact:
-            raise NotImplementedError("row bands: sparse mean outside the exact guard (gather the full map)")
+        if not exact or self.force_sequential_mean:
+            # outside the exactness guard the bands' partial sums may round
+            # differently from the reference's row-major sum (densify.cpp:60-68):
+            # gather the whole sparse map and take the sequential mean of it
+            mean = self._sequential_mean(L.gather_rows(sparse))
         self._mean = mean
         # assembly of each band's rows (+ 2-row halo)
         systems, anchors, const = {}, {}, {}
@@ -233,6 +254,17 @@ class RowBandFrames:
         out = (ctypes.c_double * 4)()
         dco._call(dco._lib().dco_band_sparse_stats, dco._p(rows), rows.numel(), out)
         return list(out)
+
+    @staticmethod
+    def _sequential_mean(full):
+        """sparse_mean (densify.cpp:60-68) of the whole map: dco_sparse_mean,
+        whose device path sums in row-major order whenever the guard fails."""
+        import ctypes
+
+        full = full.contiguous()
+        mean = ctypes.c_double()
+        dco._call(dco._lib().dco_sparse_mean, dco._p(full), full.numel(), ctypes.byref(mean))
+        return mean.value
 
     @staticmethod
     def _combine(allstats):

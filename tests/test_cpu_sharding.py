@@ -77,8 +77,10 @@ def _band_links_worker(rank, world, port, out):
         links.put_carry((rank, 0), torch.arange(6, dtype=torch.float64) + 10.0 * rank)
     stats = links.gather_stats({rank: [1.0 + rank, 2.0 * rank, 3.0, -24.0 - rank]})
     blobs = links.gather_bytes({rank: bytes([rank]) * 128})
+    # bands of different heights (rank + 2 rows of 5): the whole map in band order
+    rows = links.gather_rows({rank: torch.full((rank + 2, 5), float(rank), dtype=torch.float32)}).tolist()
     g.close()
-    out.put((rank, got, stats, blobs))
+    out.put((rank, got, stats, blobs, rows))
 
 
 def test_band_links_two_and_three_ranks():
@@ -93,7 +95,8 @@ def test_band_links_two_and_three_ranks():
         for p in ps:
             p.join(timeout=60)
             assert p.exitcode == 0
-        for rank, got, stats, blobs in res:
+        for rank, got, stats, blobs, rows in res:
+            assert rows == [[float(r)] * 5 for r in range(world) for _ in range(r + 2)]
             # band k receives exactly band k-1's carry
             assert got == (None if rank == 0 else [10.0 * (rank - 1) + i for i in range(6)])
             # every rank holds every band's statistics, rank-ordered

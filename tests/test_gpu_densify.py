@@ -246,3 +246,82 @@ def test_run_streams_equals_individual_pushes(gpu, ref):
                               N(gpu.view_tensor(getattr(b, name), shape, dt))), name
     for s in batched + single:
         s.close()
+
+
+def test_stream_unsolvable_frames(gpu, ref):
+    """pipeline.cpp:236-242: a frame with no sparse anchor and no previous
+    dense map (UnsolvableFrameError) composites against an all-nodata dense
+    map, counts the failure and leaves the d_pre chain empty; the next
+    solvable frame then starts without d_pre. (With a previous dense map every
+    pixel carries the stability term, densify.cpp:85-91, so a frame is
+    unsolvable only before the first solve.) Flat gray frames give a WTA
+    disparity of 0 everywhere, hence no sparse depth."""
+    W, H = 320, 192
+    cfg = Config(d_max=47)
+    flat8 = np.full((H, W), 128, np.uint8)
+    flat = {"left8": flat8, "right8": flat8}
+    flat["left"] = flat["right"] = ref.quantize8(flat8.astype(np.float32) / np.float32(255.0))[1]
+    fs = [flat, flat, flat] + [scene(ref, W, H, index=i, seed=4242) for i in range(3, 6)]
+    vrgb, vdepth = ref.render_cube(W, H, cfg.focal_px, cz=1.5, side=0.3)
+    s = gpu.Stream(W, H, cfg)
+    s.set_virtual(T(vrgb), T(vdepth))
+    prev = None
+    skipped = []
+    for i, f in enumerate(fs):
+        res = s.push_gray8(T(f["left8"]), T(f["right8"]))
+        if i < 2:
+            continue
+        q = [ref.downsample_half(fs[j]["left"]) for j in (i - 2, i - 1, i)]
+        mid = fs[i - 1]
+        want = ref.pipeline_frame(q[0], q[1], q[2], mid["left"], ref.downsample_half(mid["right"]),
+                                  np.repeat(mid["left"][:, :, None], 3, 2), prev, vrgb, vdepth, cfg)
+        v = s.views()
+        dense = N(gpu.view_tensor(v.dense, (H, W), torch.float32))
+        assert bool(res.densify_skipped) == want["unsolvable"]
+        skipped.append(want["unsolvable"])
+        if want["unsolvable"]:
+            assert bits_equal(dense, want["dense"])  # the nodata map
+        else:
+            d = np.abs(dense.astype(np.float64) - want["dense"])
+            assert d.max() <= MAX_ABS
+            assert abs(res.densify_iterations - want["iterations"]) <= 2
+            prev = want["dense"]
+        mask = N(gpu.view_tensor(v.mask, (H, W), torch.uint8))
+        comp = N(gpu.view_tensor(v.composite, (H, W, 3), torch.float32))
+        close = np.abs(vdepth - want["dense"]) <= 2 * MAX_ABS
+        assert ((mask == want["mask"]) | close).all()
+        assert bits_equal(comp[~close], want["composite"][~close])
+    assert skipped == [True, True, False, False]
+    s.close()
+
+
+def test_stream_save_load_state(gpu, ref):
+    """dco_stream_save_state / load_state: a fresh stream loaded with another
+    stream's state (keyframe window, previous dense map, frame counter)
+    produces the same next frame, bit for bit."""
+    from paper_2203_02300_b200.synth import StereoVideo
+
+    W, H = 320, 192
+    cfg = Config(d_max=31)
+    vid = StereoVideo(W, H, seed=555)
+    frames = [vid.frame(i) for i in range(6)]
+    a = gpu.Stream(W, H, cfg)
+    for l8, r8 in frames[:4]:
+        a.push_gray8(T(l8), T(r8))
+    torch.cuda.synchronize()
+    blob = a.state()
+    b = gpu.Stream(W, H, cfg)
+    b.load_state(blob)
+    for l8, r8 in frames[4:]:
+        ra = a.push_gray8(T(l8), T(r8))
+        rb = b.push_gray8(T(l8), T(r8))
+        assert (ra.composited, ra.densify_iterations) == (rb.composited, rb.densify_iterations)
+        va, vb = a.views(), b.views()
+        for name, shape, dt in (("dense", (H, W), torch.float32), ("composite", (H, W, 3), torch.float32),
+                                ("edges", (H, W), torch.uint8), ("sparse", (H, W), torch.float32)):
+            assert bits_equal(N(gpu.view_tensor(getattr(va, name), shape, dt)),
+                              N(gpu.view_tensor(getattr(vb, name), shape, dt))), name
+    with pytest.raises(InputError):
+        b.load_state(blob[:-8])  # truncated state
+    a.close()
+    b.close()

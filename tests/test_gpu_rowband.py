@@ -15,14 +15,18 @@ from tests.test_gpu_stereo import N, T, bits_equal
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("bands,chunk", [(1, None), (2, None), (3, 32), (5, 64)])
-def test_rowband_frames_match_reference(gpu, ref, bands, chunk):
-    """chunk: the carry travels in slice chunks (as under torchrun)."""
+@pytest.mark.parametrize("bands,chunk,seq_mean", [(1, None, False), (2, None, False), (3, 32, False), (5, 64, False),
+                                                  (3, None, True)])
+def test_rowband_frames_match_reference(gpu, ref, bands, chunk, seq_mean):
+    """chunk: the carry travels in slice chunks (as under torchrun). seq_mean:
+    the frame-wide sparse mean through the gathered-map sequential path (the
+    one taken outside the exactness guard) instead of the bands' partials."""
     W, H = 640, 360
     cfg = Config(d_max=47)
     fs = [scene(ref, W, H, index=i, seed=91) for i in range(5)]
     q = [ref.downsample_half(f["left"]) for f in fs]
     rb = RowBandFrames(W, H, cfg, LocalLinks(bands), chunk=chunk)
+    rb.force_sequential_mean = seq_mean
     prev = None
     for i in range(1, 4):
         mid = fs[i]
