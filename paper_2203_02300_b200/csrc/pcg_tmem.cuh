@@ -58,26 +58,15 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 // explicit 32-bit shared-window accesses: base register + immediate, so the
 // compiler neither rematerialises the window base per access nor spends a
 // register per array
-//
-// The loads are plain asm (no volatile, no memory clobber) so the compiler
-// may batch and reorder them: every address they use is re-issued through
-// sh_launder() after the CTA barrier that orders it against the stores of
-// other threads, which keeps them from being hoisted above that barrier or
-// out of the iteration loop. A store and a later load of the same slot by
-// the same thread are ordered by their data dependence.
 template <int IMM>
 __device__ __forceinline__ double lds(uint32_t a) {
     double v;
-    asm("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(IMM));
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(IMM) : "memory");
     return v;
 }
 template <int IMM>
 __device__ __forceinline__ void sts(uint32_t a, double v) {
-    asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(IMM), "d"(v));
-}
-__device__ __forceinline__ uint32_t sh_launder(uint32_t a) {
-    asm volatile("" : "+r"(a)::"memory");
-    return a;
+    asm volatile("st.shared.f64 [%0+%1], %2;" ::"r"(a), "n"(IMM), "d"(v) : "memory");
 }
 template <int K, int N, typename F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -110,18 +99,15 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
     const int size = qn + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int nv = size > t ? (size - t + THREADS - 1) / THREADS : 0;  // occupied slots
-    // EPT = ceil(chunk / THREADS) and size >= chunk - 1 >= (EPT - 1) * THREADS: every
-    // slot but the last is occupied for every thread (the dispatch guarantees it)
-    if (nv < EPT - 1) __builtin_unreachable();
     double* s_p = sx + w + t;
     double* s_ch = sx + 2 * w + chunk + t;
     double* s_cv = sx + 2 * w + 2 * chunk + t;
     double* s_pr = sx + 2 * w + 3 * chunk + t;
     // shared-window byte addresses of this thread's slot 0 (loop accesses)
-    const uint32_t aP0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_p));
-    const uint32_t aCH0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_ch));
-    const uint32_t aCV0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_cv));
-    const uint32_t aPR0 = static_cast<uint32_t>(__cvta_generic_to_shared(s_pr));
+    const uint32_t aP = static_cast<uint32_t>(__cvta_generic_to_shared(s_p));
+    const uint32_t aCH = static_cast<uint32_t>(__cvta_generic_to_shared(s_ch));
+    const uint32_t aCV = static_cast<uint32_t>(__cvta_generic_to_shared(s_cv));
+    const uint32_t aPR = static_cast<uint32_t>(__cvta_generic_to_shared(s_pr));
     const uint32_t wb = 8u * static_cast<uint32_t>(w);
     unsigned gen = 0;
     double r[EPT], x[EPT];
@@ -306,7 +292,6 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
 #pragma unroll
             for (int c = 0; c < 10; ++c) v[c] = 0.0;
             tm_wait_st();  // last phase's q / xs / rs stores have landed
-            const uint32_t aP = sh_launder(aP0), aPR = sh_launder(aPR0);
             static_for<0, EPT>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
                 uint32_t c4[4], c2[2], cx[2];
@@ -370,8 +355,6 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
             __syncthreads();
             STAMP(5)
             // P2: q = A p -- stencil order of densify.cpp:125-129; pq, S2, S3, T2, U2, U3
-            const uint32_t aP = sh_launder(aP0), aPR = sh_launder(aPR0), aCH = sh_launder(aCH0),
-                           aCV = sh_launder(aCV0);
             uint32_t cur4[4];
             tm_ld4(tm + 4, cur4);  // rs, diag of slot 0
             tm_wait_ld();
