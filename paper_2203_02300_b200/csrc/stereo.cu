@@ -1778,7 +1778,9 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
                                 kHcThreads, static_cast<size_t>(nbp) * kHcThreads, ctx->stream>>>(src, w, h, l, r,
                                                                                                   nbp, hcnt);
             launched(ctx, "k_refine_hscatter");
-            const int seg = packed ? 64 : 32, nseg = (h + seg - 1) / seg;
+            int seg = packed ? 64 : 32;
+            if (const char* e = getenv("DCO_REFINE_SEG")) seg = std::max(8, atoi(e));  // tuning hook
+            const int nseg = (h + seg - 1) / seg;
             unsigned* carry = static_cast<unsigned*>(scratch(ctx, S_TMP1, static_cast<size_t>(w) * nseg * nbp * 4));
             dim3 vb(32 * vwarps), vg((w * nseg + vwarps - 1) / vwarps);
             if (packed) {
