@@ -14,7 +14,7 @@
  * 2.35 hypot kernel without FMA; fdlibm atanf/atan2f). Constants are the
  * algorithms' published constants; the 128-entry exp table is regenerated
  * from its definition (oracle/gen_exp_table.py, which checks it against the
- * host libm). tests/test_libm_replica.py pins every routine against the host
+ * host libm). tests/test_cpu_boundary.py (with oracle/libm_check.c) pins every routine against the host
  * libm on large random + edge-case sweeps (exhaustively for the exp argument
  * domain the cost volume uses).
  *

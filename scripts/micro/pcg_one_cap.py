@@ -1,5 +1,6 @@
 """Solves the bench frame's system with an iteration cap and saves the dense
-map (for comparing solver variants across processes)."""
+map (for comparing solver variants across processes). The system comes from
+system_1280x720.npz, written by scripts/micro/dump_system.py (not tracked)."""
 import os
 import sys
 
