@@ -946,6 +946,126 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_refine_thread(
     }
 }
 
+// ---------------------------------------------------------------------------
+// Histogram refinement by region extrema (stereo.cpp:240-299), the frame
+// loop's default. The refined map is piecewise constant: at config B 90 % of
+// the cross regions hold a single distinct disparity (95 % at most two). For
+// such a region the histogram has one bin, its count is the region's valid
+// count, so the mode is that value and "mode_count == 1 && region >= 4" cannot
+// hold. So:
+//   k_ref_hminmax : per pixel (x, y'), the min / max bin over its horizontal
+//                   span in row y' (NaN skipped; empty -> min > max);
+//   k_ref_vminmax : per pixel (x, y), the min / max over its vertical arm of
+//                   those; a valid centre with min == max takes that bin; any
+//                   other valid centre is queued (warp-aggregated atomic);
+//   k_ref_slow    : warp per queued pixel: the exact histogram of its region
+//                   in shared memory (lanes over a span, __match_any_sync
+//                   groups equal bins so each distinct bin is added once per
+//                   row chunk), then the (count, smallest bin) argmax over
+//                   [lo, hi] and the reference's outlier rule.
+// Min, max and counts are exact integers in any order, so every output is the
+// reference's. A NaN centre stays NaN (stereo.cpp:258).
+__global__ void k_ref_hminmax(const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ L,
+                              const uint8_t* __restrict__ R, int cap, short2* __restrict__ mm) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= w) return;
+    const size_t i = static_cast<size_t>(y) * w + x;
+    const float* row = cur + static_cast<size_t>(y) * w;
+    int lo = 0x7fff, hi = -1;
+    for (int c = x - L[i], e = x + R[i]; c <= e; ++c) {
+        const float v = row[c];
+        if (!isfinite(v)) continue;
+        const int b = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
+        lo = min(lo, b);
+        hi = max(hi, b);
+    }
+    mm[i] = make_short2(static_cast<short>(lo), static_cast<short>(hi));
+}
+
+__global__ void k_ref_vminmax(const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ U,
+                              const uint8_t* __restrict__ D, const short2* __restrict__ mm,
+                              float* __restrict__ next, int* __restrict__ queue) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= w) return;
+    const size_t i = static_cast<size_t>(y) * w + x;
+    const float c = cur[i];
+    if (!isfinite(c)) {  // removed outliers stay removed
+        next[i] = c;
+        return;
+    }
+    int lo = 0x7fff, hi = -1;
+    for (int yy = y - U[i], ye = y + D[i]; yy <= ye; ++yy) {
+        const short2 v = mm[static_cast<size_t>(yy) * w + x];
+        lo = min(lo, static_cast<int>(v.x));
+        hi = max(hi, static_cast<int>(v.y));
+    }
+    if (lo == hi) {
+        next[i] = static_cast<float>(lo);
+    } else {
+        queue[1 + atomicAdd(queue, 1)] = static_cast<int>(i);
+    }
+}
+
+constexpr int kSlowWarps = 8;
+__global__ void __launch_bounds__(kSlowWarps * 32) k_ref_slow(const float* __restrict__ cur, int w, int h,
+                                                              const uint8_t* __restrict__ L,
+                                                              const uint8_t* __restrict__ R,
+                                                              const uint8_t* __restrict__ U,
+                                                              const uint8_t* __restrict__ D, int cap,
+                                                              const int* __restrict__ queue,
+                                                              float* __restrict__ next) {
+    extern __shared__ unsigned short rs_hist[];  // [kSlowWarps][cap]
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    unsigned short* hist = rs_hist + static_cast<size_t>(wp) * cap;
+    for (int b = lane; b < cap; b += 32) hist[b] = 0;
+    __syncwarp();
+    const int nq = queue[0];
+    for (int q = blockIdx.x * kSlowWarps + wp; q < nq; q += gridDim.x * kSlowWarps) {
+        const int i = queue[1 + q];
+        const int y = i / w, x = i - y * w;
+        int lo = 0x7fff, hi = -1, total = 0;
+        for (int yy = y - U[i], ye = y + D[i]; yy <= ye; ++yy) {
+            const size_t vi = static_cast<size_t>(yy) * w + x;
+            const float* row = cur + static_cast<size_t>(yy) * w;
+            const int a = x - L[vi], e = x + R[vi];
+            for (int c0 = a; c0 <= e; c0 += 32) {
+                const int c = c0 + lane;
+                int b = -1;
+                if (c <= e) {
+                    const float v = row[c];
+                    if (isfinite(v)) b = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
+                }
+                const unsigned grp = __match_any_sync(0xffffffffu, b);
+                if (b >= 0) {
+                    const int leader = __ffs(grp) - 1;
+                    if (lane == leader) hist[b] = static_cast<unsigned short>(hist[b] + __popc(grp));
+                    lo = min(lo, b);
+                    hi = max(hi, b);
+                    ++total;
+                }
+                __syncwarp();
+            }
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(hi + 1)) - 1;
+        total = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(total)));
+        // (count, smallest bin) argmax: the reference's strict '>' scan from lo (stereo.cpp:272-278)
+        unsigned key = 0;
+        for (int b = lo + lane; b <= hi; b += 32) {
+            const unsigned cnt = hist[b];
+            if (cnt) key = max(key, (cnt << 16) | (0xffffu - static_cast<unsigned>(b)));
+            hist[b] = 0;
+        }
+        key = __reduce_max_sync(0xffffffffu, key);
+        if (lane == 0) {
+            const int best_c = static_cast<int>(key >> 16);
+            const int best_b = static_cast<int>(0xffffu - (key & 0xffffu));
+            next[i] = (best_c == 1 && total >= 4) ? __int_as_float(0x7fc00000) : static_cast<float>(best_b);
+        }
+        __syncwarp();
+    }
+}
+
 // Histogram refinement as an exact integer cross-aggregation (the region
 // histogram of stereo.cpp:252-297 is the cross-region sum of one-hot bins):
 //   H(x, y', v) = #{c in the horizontal span of (x, y') : bin(c, y') == v}
@@ -1740,6 +1860,32 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     }
     require(cap <= 8192, "refine_disparity_histogram: disparities above 8191 are not supported");
     cap = (cap + 31) & ~31;
+    if (cap <= 4096 && !getenv("DCO_REFINE_DENSE")) {
+        // region extrema + exact histograms only where a region holds two or more bins
+        float* bufs2[2] = {static_cast<float*>(scratch(ctx, S_DISP0, n * 4)),
+                           static_cast<float*>(scratch(ctx, S_DISP1, n * 4))};
+        short2* mm = static_cast<short2*>(scratch(ctx, S_HSUM, n * sizeof(short2)));
+        int* queue = static_cast<int*>(scratch(ctx, S_TMP1, (n + 1) * sizeof(int)));
+        const int rows = 1;
+        dim3 b(128, rows);
+        dim3 g((w + 127) / 128, h);
+        const size_t hsm = static_cast<size_t>(kSlowWarps) * cap * sizeof(unsigned short);
+        smem_attr(ctx, k_ref_slow, static_cast<int>(hsm));
+        const float* src = disp;
+        for (int it = 0; it < iters; ++it) {
+            float* dst = (it == iters - 1) ? out : bufs2[it & 1];
+            k_ref_hminmax<<<g, b, 0, ctx->stream>>>(src, w, h, l, r, cap, mm);
+            launched(ctx, "k_ref_hminmax");
+            cuda_check(cudaMemsetAsync(queue, 0, sizeof(int), ctx->stream), "memset");
+            k_ref_vminmax<<<g, b, 0, ctx->stream>>>(src, w, h, u, d, mm, dst, queue);
+            launched(ctx, "k_ref_vminmax");
+            k_ref_slow<<<sm_count(ctx) * 4, kSlowWarps * 32, hsm, ctx->stream>>>(src, w, h, l, r, u, d, cap, queue,
+                                                                                 dst);
+            launched(ctx, "k_ref_slow");
+            src = dst;
+        }
+        return;
+    }
     const int warps = 8;
     const int rows_cap = 2 * max_arm + 2;
     size_t smem = static_cast<size_t>(warps) * (cap + 3 * rows_cap + 1) * sizeof(unsigned);
