@@ -966,24 +966,52 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_refine_thread(
 // Min, max and counts are exact integers in any order, so every output is the
 // reference's. A NaN centre stays NaN (stereo.cpp:258).
 __global__ void k_ref_hminmax(const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ L,
-                              const uint8_t* __restrict__ R, int cap, short2* __restrict__ mm) {
+                              const uint8_t* __restrict__ R, int cap, uint2* __restrict__ mm) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
     if (x >= w) return;
     const size_t i = static_cast<size_t>(y) * w + x;
     const float* row = cur + static_cast<size_t>(y) * w;
-    int lo = 0x7fff, hi = -1;
+    // the span's distinct bins, up to two (a < b), their counts, and whether a third exists
+    int a = 0x7fff, b = -1, ca = 0, cb = 0;
+    bool three = false;
     for (int c = x - L[i], e = x + R[i]; c <= e; ++c) {
         const float v = row[c];
         if (!isfinite(v)) continue;
-        const int b = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
-        lo = min(lo, b);
-        hi = max(hi, b);
+        const int bin = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
+        if (bin == a) {
+            ++ca;
+        } else if (bin == b) {
+            ++cb;
+        } else if (b < 0) {  // a second distinct bin (or the first)
+            if (a == 0x7fff) {
+                a = bin;
+                ca = 1;
+            } else if (bin < a) {
+                b = a;
+                cb = ca;
+                a = bin;
+                ca = 1;
+            } else {
+                b = bin;
+                cb = 1;
+            }
+        } else {
+            three = true;
+            a = min(a, bin);
+            b = max(b, bin);
+        }
     }
-    mm[i] = make_short2(static_cast<short>(lo), static_cast<short>(hi));
+    if (b < 0 && a != 0x7fff) {  // one distinct bin: min == max
+        b = a;
+        cb = ca;
+    }
+    mm[i] = make_uint2(static_cast<uint32_t>(a & 0xffff) | (static_cast<uint32_t>(b & 0xffff) << 16),
+                       static_cast<uint32_t>(min(ca, 255)) | (static_cast<uint32_t>(min(cb, 255)) << 8) |
+                           (three ? 1u << 16 : 0u));
 }
 
 __global__ void k_ref_vminmax(const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ U,
-                              const uint8_t* __restrict__ D, const short2* __restrict__ mm,
+                              const uint8_t* __restrict__ D, const uint2* __restrict__ mm,
                               float* __restrict__ next, int* __restrict__ queue) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
     if (x >= w) return;
@@ -993,17 +1021,39 @@ __global__ void k_ref_vminmax(const float* __restrict__ cur, int w, int h, const
         next[i] = c;
         return;
     }
+    const int y0 = y - U[i], y1 = y + D[i];
     int lo = 0x7fff, hi = -1;
-    for (int yy = y - U[i], ye = y + D[i]; yy <= ye; ++yy) {
-        const short2 v = mm[static_cast<size_t>(yy) * w + x];
-        lo = min(lo, static_cast<int>(v.x));
-        hi = max(hi, static_cast<int>(v.y));
+    bool three = false;
+    for (int yy = y0; yy <= y1; ++yy) {
+        const uint2 v = mm[static_cast<size_t>(yy) * w + x];
+        lo = min(lo, static_cast<int>(v.x & 0xffffu));
+        hi = max(hi, static_cast<int>(static_cast<short>(v.x >> 16)));
+        three |= (v.y >> 16) != 0;
     }
-    if (lo == hi) {
+    if (lo == hi) {  // one bin in the region: it is the mode
         next[i] = static_cast<float>(lo);
-    } else {
-        queue[1 + atomicAdd(queue, 1)] = static_cast<int>(i);
+        return;
     }
+    if (!three) {
+        // two bins lo < hi, if every span holds only those: counts from the spans,
+        // the mode is lo on ties (smaller bin) and "mode_count == 1 && region >= 4"
+        // cannot hold (both counts 1 means a region of 2)
+        bool two = true;
+        int nlo = 0, nhi = 0;
+        for (int yy = y0; yy <= y1; ++yy) {
+            const uint2 v = mm[static_cast<size_t>(yy) * w + x];
+            const int a = static_cast<int>(v.x & 0xffffu), b = static_cast<int>(static_cast<short>(v.x >> 16));
+            if (b < 0) continue;  // no valid value in this span
+            two &= (a == lo || a == hi) && (b == lo || b == hi);
+            nlo += a == lo ? static_cast<int>(v.y & 255u) : 0;
+            nhi += b == hi ? static_cast<int>((v.y >> 8) & 255u) : 0;
+        }
+        if (two) {
+            next[i] = static_cast<float>(nlo >= nhi ? lo : hi);
+            return;
+        }
+    }
+    queue[1 + atomicAdd(queue, 1)] = static_cast<int>(i);
 }
 
 constexpr int kSlowWarps = 8;
@@ -1024,26 +1074,35 @@ __global__ void __launch_bounds__(kSlowWarps * 32) k_ref_slow(const float* __res
         const int i = queue[1 + q];
         const int y = i / w, x = i - y * w;
         int lo = 0x7fff, hi = -1, total = 0;
-        for (int yy = y - U[i], ye = y + D[i]; yy <= ye; ++yy) {
-            const size_t vi = static_cast<size_t>(yy) * w + x;
-            const float* row = cur + static_cast<size_t>(yy) * w;
-            const int a = x - L[vi], e = x + R[vi];
-            for (int c0 = a; c0 <= e; c0 += 32) {
-                const int c = c0 + lane;
-                int b = -1;
-                if (c <= e) {
-                    const float v = row[c];
-                    if (isfinite(v)) b = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
+        const int y0 = y - U[i], nrow = y + D[i] - y0 + 1;
+        for (int r0 = 0; r0 < nrow; r0 += 32) {
+            // lane j holds the span of row y0 + r0 + j (one load round for 32 rows)
+            int sa = 0, se = -1;
+            if (r0 + lane < nrow) {
+                const size_t vi = static_cast<size_t>(y0 + r0 + lane) * w + x;
+                sa = x - L[vi];
+                se = x + R[vi];
+            }
+            const int rn = min(32, nrow - r0);
+            for (int rr = 0; rr < rn; ++rr) {
+                const int a = __shfl_sync(0xffffffffu, sa, rr), e = __shfl_sync(0xffffffffu, se, rr);
+                const float* row = cur + static_cast<size_t>(y0 + r0 + rr) * w;
+                for (int c0 = a; c0 <= e; c0 += 32) {
+                    const int c = c0 + lane;
+                    int b = -1;
+                    if (c <= e) {
+                        const float v = row[c];
+                        if (isfinite(v)) b = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
+                    }
+                    const unsigned grp = __match_any_sync(0xffffffffu, b);
+                    if (b >= 0) {
+                        if (lane == __ffs(grp) - 1) hist[b] = static_cast<unsigned short>(hist[b] + __popc(grp));
+                        lo = min(lo, b);
+                        hi = max(hi, b);
+                        ++total;
+                    }
+                    __syncwarp();
                 }
-                const unsigned grp = __match_any_sync(0xffffffffu, b);
-                if (b >= 0) {
-                    const int leader = __ffs(grp) - 1;
-                    if (lane == leader) hist[b] = static_cast<unsigned short>(hist[b] + __popc(grp));
-                    lo = min(lo, b);
-                    hi = max(hi, b);
-                    ++total;
-                }
-                __syncwarp();
             }
         }
         lo = __reduce_min_sync(0xffffffffu, lo);
@@ -1860,11 +1919,11 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     }
     require(cap <= 8192, "refine_disparity_histogram: disparities above 8191 are not supported");
     cap = (cap + 31) & ~31;
-    if (cap <= 4096 && !getenv("DCO_REFINE_DENSE")) {
+    if (cap <= 4096 && max_arm <= 127 && !getenv("DCO_REFINE_DENSE")) {  // span counts fit a byte
         // region extrema + exact histograms only where a region holds two or more bins
         float* bufs2[2] = {static_cast<float*>(scratch(ctx, S_DISP0, n * 4)),
                            static_cast<float*>(scratch(ctx, S_DISP1, n * 4))};
-        short2* mm = static_cast<short2*>(scratch(ctx, S_HSUM, n * sizeof(short2)));
+        uint2* mm = static_cast<uint2*>(scratch(ctx, S_HSUM, n * sizeof(uint2)));
         int* queue = static_cast<int*>(scratch(ctx, S_TMP1, (n + 1) * sizeof(int)));
         const int rows = 1;
         dim3 b(128, rows);
