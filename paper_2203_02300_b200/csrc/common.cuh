@@ -125,6 +125,61 @@ inline unsigned blocks_for(size_t n, unsigned threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);
 }
 
+#ifdef __CUDACC__
+// One global atomic per BLOCK instead of one per warp: same-address atomics
+// serialise at their L2 slice, so a per-warp atomic over a full-frame grid
+// (28 800 warps at 1280x720) costs more than the kernel's own work. Every
+// thread of the block must call these (they contain __syncthreads); v is the
+// thread's value, `skip` the identity the global update is not issued for.
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce_lane(T v, Op op, T ident) {
+    __shared__ T s_red[32];
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nw = (blockDim.x * blockDim.y * blockDim.z + 31) >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if ((tid & 31) == 0) s_red[tid >> 5] = v;
+    __syncthreads();
+    T r = ident;
+    if (tid < 32) {
+        r = tid < nw ? s_red[tid] : ident;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) r = op(r, __shfl_xor_sync(0xffffffffu, r, off));
+    }
+    __syncthreads();  // s_red reusable
+    return r;  // valid in thread 0
+}
+struct OpMax {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return a > b ? a : b; }
+};
+struct OpMin {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return a < b ? a : b; }
+};
+struct OpAdd {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return a + b; }
+};
+__device__ __forceinline__ bool block_leader() { return (threadIdx.x | threadIdx.y | threadIdx.z) == 0; }
+__device__ __forceinline__ void block_atomic_max(unsigned* g, unsigned v) {
+    const unsigned r = block_reduce_lane(v, OpMax{}, 0u);
+    if (block_leader() && r) atomicMax(g, r);
+}
+__device__ __forceinline__ void block_atomic_max(int* g, int v) {
+    const int r = block_reduce_lane(v, OpMax{}, 0);
+    if (block_leader() && r > 0) atomicMax(g, r);
+}
+__device__ __forceinline__ void block_atomic_min(int* g, int v, int ident) {
+    const int r = block_reduce_lane(v, OpMin{}, ident);
+    if (block_leader() && r != ident) atomicMin(g, r);
+}
+__device__ __forceinline__ void block_atomic_add(unsigned long long* g, unsigned long long v) {
+    const unsigned long long r = block_reduce_lane(v, OpAdd{}, 0ull);
+    if (block_leader() && r) atomicAdd(g, r);
+}
+#endif
+
 // The C-ABI edge: runs fn, maps Failure/std::exception to status codes.
 template <typename F>
 int guarded(dco_ctx* ctx, F&& fn) {

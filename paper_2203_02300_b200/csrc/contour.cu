@@ -216,9 +216,7 @@ __global__ void k_peak(const float* __restrict__ a, size_t n, unsigned* __restri
         float v = a[i];
         if (isfinite(v) && v > 0.0f) b = __float_as_uint(v);
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, off));
-    if ((threadIdx.x & 31) == 0 && b) atomicMax(peak_bits, b);
+    block_atomic_max(peak_bits, b);
 }
 // normalize_amplitude, contour.cpp:138-147.
 __global__ void k_normalize(const float* __restrict__ a, size_t n, const unsigned* __restrict__ peak_bits,
@@ -280,9 +278,7 @@ __global__ void k_sobel(const float* __restrict__ b, int w, int h, float* __rest
         mag[i] = m;
         if (m > 0.0f) pb = __float_as_uint(m);  // NaN-free: inputs finite
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) pb = max(pb, __shfl_xor_sync(0xffffffffu, pb, off));
-    if ((threadIdx.x + threadIdx.y * blockDim.x) % 32 == 0 && pb) atomicMax(peak_bits, pb);
+    block_atomic_max(peak_bits, pb);
 }
 
 // contour.cpp:197-203: mag /= peak (peak > 0), copied out as m_i.

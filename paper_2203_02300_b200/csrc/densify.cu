@@ -162,17 +162,24 @@ __global__ void k_sparse_stats(const float* __restrict__ s, size_t n, double* __
     double v[2] = {0.0, 0.0};
     unsigned long long c = 0;
     int me = 1 << 20;
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        float f = s[i];
-        if (isfinite(f)) {
-            v[0] += f;
-            v[1] += fabs(static_cast<double>(f));
-            ++c;
-            if (f != 0.0f) {
-                int e;
-                frexpf(f, &e);  // f = m * 2^e, m in [0.5,1): ulp = 2^(e-24), denormal-safe bound
-                me = min(me, max(e - 24, -149));
+    constexpr int kB = 4;  // loads of kB elements in flight, grid-stride order kept
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += kB * stride) {
+        float fs[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) fs[j] = i0 + j * stride < n ? s[i0 + j * stride] : __int_as_float(0x7fc00000);
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const float f = fs[j];
+            if (isfinite(f)) {
+                v[0] += f;
+                v[1] += fabs(static_cast<double>(f));
+                ++c;
+                if (f != 0.0f) {
+                    int e;
+                    frexpf(f, &e);  // f = m * 2^e, m in [0.5,1): ulp = 2^(e-24), denormal-safe bound
+                    me = min(me, max(e - 24, -149));
+                }
             }
         }
     }
@@ -181,14 +188,8 @@ __global__ void k_sparse_stats(const float* __restrict__ s, size_t n, double* __
         part[2 * blockIdx.x] = v[0];
         part[2 * blockIdx.x + 1] = v[1];
     }
-    for (int off = 16; off > 0; off >>= 1) {
-        c += __shfl_xor_sync(0xffffffffu, c, off);
-        me = min(me, __shfl_xor_sync(0xffffffffu, me, off));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (c) atomicAdd(count, c);
-        atomicMin(min_exp, me);
-    }
+    block_atomic_add(count, c);
+    block_atomic_min(min_exp, me, 1 << 20);
 }
 
 // Finishes the sparse mean (densify.cpp:60-68): exact tree when the guard
@@ -232,26 +233,37 @@ __global__ void k_anchor_const(const uint8_t* __restrict__ anch, const float* __
     if (pre && pre_valid && *pre_valid == 0) pre = nullptr;
     double v[1] = {0.0};
     unsigned long long c = 0;
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        c += anch[i];
-        float f = s[i];
-        if (isfinite(f)) {
-            double ds = f;
-            v[0] += ld * ds * ds;
+    // the thread's elements in the same order as a plain grid-stride loop,
+    // with the loads of kB of them issued before any is used
+    constexpr int kB = 4;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    for (size_t i0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += kB * stride) {
+        float f[kB], g[kB];
+        unsigned a[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const size_t i = i0 + j * stride;
+            const bool in = i < n;
+            a[j] = in ? anch[i] : 0u;
+            f[j] = in ? s[i] : __int_as_float(0x7fc00000);
+            g[j] = in && pre ? pre[i] : __int_as_float(0x7fc00000);
         }
-        if (pre) {
-            float g = pre[i];
-            if (isfinite(g)) {
-                double dp = g;
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            c += a[j];
+            if (isfinite(f[j])) {
+                double ds = f[j];
+                v[0] += ld * ds * ds;
+            }
+            if (isfinite(g[j])) {
+                double dp = g[j];
                 v[0] += ls2 * dp * dp;
             }
         }
     }
     block_sum<1>(v, sm);
     if (threadIdx.x == 0) part[blockIdx.x] = v[0];
-    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+    block_atomic_add(count, c);
 }
 
 // (sum, |sum|) of k_sparse_stats' block partials

@@ -776,9 +776,7 @@ __global__ void k_bin_max(const float* __restrict__ disp, int n, int* __restrict
         float v = disp[i];
         if (isfinite(v)) b = max(0, static_cast<int>(lroundf(v)));
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, off));
-    if ((threadIdx.x & 31) == 0 && b > 0) atomicMax(out, b);
+    block_atomic_max(out, b);
 }
 
 // One warp per pixel (grid-stride over pixels). The cross region — the
@@ -1649,9 +1647,7 @@ __global__ void k_max_arm(const uint8_t* __restrict__ a0, const uint8_t* __restr
     size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     int m = 0;
     if (i < n) m = max(max(a0[i], a1[i]), max(a2[i], a3[i]));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out, m);
+    block_atomic_max(out, m);
 }
 
 inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
