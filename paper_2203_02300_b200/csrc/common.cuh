@@ -81,6 +81,7 @@ enum Slot : int {
     S_FIXLIST,
     S_BADROW,
     S_EXPORT,
+    S_RUNS,
     S_COUNT
 };
 

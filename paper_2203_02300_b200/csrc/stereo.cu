@@ -963,40 +963,80 @@ __global__ void __launch_bounds__(kHistThreads) k_hist_refine_thread(
 //                   [lo, hi] and the reference's outlier rule.
 // Min, max and counts are exact integers in any order, so every output is the
 // reference's. A NaN centre stays NaN (stereo.cpp:258).
-__global__ void k_ref_hminmax(const float* __restrict__ cur, int w, int h, const uint8_t* __restrict__ L,
-                              const uint8_t* __restrict__ R, int cap, uint2* __restrict__ mm) {
+// Row runs of equal bins (NaN = bin -1): runs[y][x] = bin(x) & 0xffff |
+// (last x' of the run holding x) << 16. The region scans below then step from
+// run to run instead of from pixel to pixel: the refined map is piecewise
+// constant, so a 35-pixel span is typically one to three runs.
+__device__ __forceinline__ int ref_bin(float v, int cap) {
+    return isfinite(v) ? min(max(static_cast<int>(lroundf(v)), 0), cap - 1) : -1;
+}
+__global__ void k_ref_runs(const float* __restrict__ cur, int w, int h, int cap, uint32_t* __restrict__ runs) {
+    extern __shared__ uint32_t rr_chg[];  // bit x: the run ends at x
+    const int y = blockIdx.x, lane = threadIdx.x & 31;
+    const float* row = cur + static_cast<size_t>(y) * w;
+    const int nwd = (w + 31) >> 5;
+    for (int x0 = 0; x0 < nwd * 32; x0 += blockDim.x) {  // uniform trip count (blockDim % 32 == 0)
+        const int x = x0 + static_cast<int>(threadIdx.x);
+        const bool c = x >= w - 1 || ref_bin(row[x], cap) != ref_bin(row[x + 1], cap);
+        const unsigned bal = __ballot_sync(0xffffffffu, c);
+        if (lane == 0 && (x >> 5) < nwd) rr_chg[x >> 5] = bal;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < w; x += blockDim.x) {
+        int wd = x >> 5;
+        unsigned m = rr_chg[wd] & (0xffffffffu << (x & 31));
+        while (!m) m = rr_chg[++wd];  // bit w - 1 is set
+        const int e = (wd << 5) + __ffs(m) - 1;
+        runs[static_cast<size_t>(y) * w + x] =
+            (static_cast<uint32_t>(ref_bin(row[x], cap)) & 0xffffu) | (static_cast<uint32_t>(e) << 16);
+    }
+}
+
+__global__ void k_ref_hminmax(const uint32_t* __restrict__ runs, int w, int h, const uint8_t* __restrict__ L,
+                              const uint8_t* __restrict__ R, uint2* __restrict__ mm) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
     if (x >= w) return;
     const size_t i = static_cast<size_t>(y) * w + x;
-    const float* row = cur + static_cast<size_t>(y) * w;
-    // the span's distinct bins, up to two (a < b), their counts, and whether a third exists
+    const uint32_t* row = runs + static_cast<size_t>(y) * w;
+    // the span's distinct bins, up to two (a < b), their counts, and whether a
+    // third exists -- the per-pixel scan's state after each run of len pixels
     int a = 0x7fff, b = -1, ca = 0, cb = 0;
     bool three = false;
-    for (int c = x - L[i], e = x + R[i]; c <= e; ++c) {
-        const float v = row[c];
-        if (!isfinite(v)) continue;
-        const int bin = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
+    for (int c = x - L[i], e = x + R[i]; c <= e;) {
+        const uint32_t v = row[c];
+        const int bin = static_cast<short>(v & 0xffffu);
+        const int end = min(static_cast<int>(v >> 16), e);
+        const int len = end - c + 1;
+        c = end + 1;
+        if (bin < 0) continue;
         if (bin == a) {
-            ++ca;
+            ca += len;
         } else if (bin == b) {
-            ++cb;
+            cb += len;
         } else if (b < 0) {  // a second distinct bin (or the first)
             if (a == 0x7fff) {
                 a = bin;
-                ca = 1;
+                ca = len;
             } else if (bin < a) {
                 b = a;
                 cb = ca;
                 a = bin;
-                ca = 1;
+                ca = len;
             } else {
                 b = bin;
-                cb = 1;
+                cb = len;
             }
         } else {
+            // a third bin: the first pixel only moves the extrema, the rest of
+            // the run then counts toward whichever extremum it became
             three = true;
             a = min(a, bin);
             b = max(b, bin);
+            if (bin == a) {
+                ca += len - 1;
+            } else if (bin == b) {
+                cb += len - 1;
+            }
         }
     }
     if (b < 0 && a != 0x7fff) {  // one distinct bin: min == max
@@ -1055,17 +1095,19 @@ __global__ void k_ref_vminmax(const float* __restrict__ cur, int w, int h, const
 }
 
 constexpr int kSlowWarps = 8;
-__global__ void __launch_bounds__(kSlowWarps * 32) k_ref_slow(const float* __restrict__ cur, int w, int h,
+__global__ void __launch_bounds__(kSlowWarps * 32) k_ref_slow(const uint32_t* __restrict__ runs, int w, int h,
                                                               const uint8_t* __restrict__ L,
                                                               const uint8_t* __restrict__ R,
                                                               const uint8_t* __restrict__ U,
                                                               const uint8_t* __restrict__ D, int cap,
                                                               const int* __restrict__ queue,
                                                               float* __restrict__ next) {
-    extern __shared__ unsigned short rs_hist[];  // [kSlowWarps][cap]
+    // per warp: cap 16-bit counts packed two per word (a region holds at most
+    // 255 x 255 pixels, so a half never carries into the other)
+    extern __shared__ uint32_t rs_hist[];  // [kSlowWarps][cap / 2]
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    unsigned short* hist = rs_hist + static_cast<size_t>(wp) * cap;
-    for (int b = lane; b < cap; b += 32) hist[b] = 0;
+    uint32_t* hist = rs_hist + static_cast<size_t>(wp) * (cap >> 1);
+    for (int b = lane; b < (cap >> 1); b += 32) hist[b] = 0;
     __syncwarp();
     const int nq = queue[0];
     for (int q = blockIdx.x * kSlowWarps + wp; q < nq; q += gridDim.x * kSlowWarps) {
@@ -1073,46 +1115,35 @@ __global__ void __launch_bounds__(kSlowWarps * 32) k_ref_slow(const float* __res
         const int y = i / w, x = i - y * w;
         int lo = 0x7fff, hi = -1, total = 0;
         const int y0 = y - U[i], nrow = y + D[i] - y0 + 1;
-        for (int r0 = 0; r0 < nrow; r0 += 32) {
-            // lane j holds the span of row y0 + r0 + j (one load round for 32 rows)
-            int sa = 0, se = -1;
-            if (r0 + lane < nrow) {
-                const size_t vi = static_cast<size_t>(y0 + r0 + lane) * w + x;
-                sa = x - L[vi];
-                se = x + R[vi];
-            }
-            const int rn = min(32, nrow - r0);
-            for (int rr = 0; rr < rn; ++rr) {
-                const int a = __shfl_sync(0xffffffffu, sa, rr), e = __shfl_sync(0xffffffffu, se, rr);
-                const float* row = cur + static_cast<size_t>(y0 + r0 + rr) * w;
-                for (int c0 = a; c0 <= e; c0 += 32) {
-                    const int c = c0 + lane;
-                    int b = -1;
-                    if (c <= e) {
-                        const float v = row[c];
-                        if (isfinite(v)) b = min(max(static_cast<int>(lroundf(v)), 0), cap - 1);
-                    }
-                    const unsigned grp = __match_any_sync(0xffffffffu, b);
-                    if (b >= 0) {
-                        if (lane == __ffs(grp) - 1) hist[b] = static_cast<unsigned short>(hist[b] + __popc(grp));
-                        lo = min(lo, b);
-                        hi = max(hi, b);
-                        ++total;
-                    }
-                    __syncwarp();
-                }
+        // lane j walks the runs of the span of row y0 + r0 + j
+        for (int r0 = lane; r0 < nrow; r0 += 32) {
+            const size_t vi = static_cast<size_t>(y0 + r0) * w + x;
+            const uint32_t* row = runs + static_cast<size_t>(y0 + r0) * w;
+            for (int c = x - L[vi], e = x + R[vi]; c <= e;) {
+                const uint32_t v = row[c];
+                const int bin = static_cast<short>(v & 0xffffu);
+                const int end = min(static_cast<int>(v >> 16), e);
+                const int len = end - c + 1;
+                c = end + 1;
+                if (bin < 0) continue;
+                atomicAdd(hist + (bin >> 1), static_cast<uint32_t>(len) << (16 * (bin & 1)));
+                lo = min(lo, bin);
+                hi = max(hi, bin);
+                total += len;
             }
         }
+        __syncwarp();
         lo = __reduce_min_sync(0xffffffffu, lo);
         hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(hi + 1)) - 1;
         total = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(total)));
         // (count, smallest bin) argmax: the reference's strict '>' scan from lo (stereo.cpp:272-278)
         unsigned key = 0;
         for (int b = lo + lane; b <= hi; b += 32) {
-            const unsigned cnt = hist[b];
+            const unsigned cnt = (hist[b >> 1] >> (16 * (b & 1))) & 0xffffu;
             if (cnt) key = max(key, (cnt << 16) | (0xffffu - static_cast<unsigned>(b)));
-            hist[b] = 0;
         }
+        __syncwarp();
+        for (int b = (lo >> 1) + lane; b <= (hi >> 1); b += 32) hist[b] = 0;
         key = __reduce_max_sync(0xffffffffu, key);
         if (lane == 0) {
             const int best_c = static_cast<int>(key >> 16);
@@ -1915,26 +1946,31 @@ void refine_disparity_histogram(dco_ctx* ctx, const float* disp, int w, int h, c
     }
     require(cap <= 8192, "refine_disparity_histogram: disparities above 8191 are not supported");
     cap = (cap + 31) & ~31;
-    if (cap <= 4096 && max_arm <= 127 && !getenv("DCO_REFINE_DENSE")) {  // span counts fit a byte
+    if (cap <= 4096 && max_arm <= 127 && w <= 65535 && !getenv("DCO_REFINE_DENSE")) {  // span counts fit a byte
         // region extrema + exact histograms only where a region holds two or more bins
         float* bufs2[2] = {static_cast<float*>(scratch(ctx, S_DISP0, n * 4)),
                            static_cast<float*>(scratch(ctx, S_DISP1, n * 4))};
         uint2* mm = static_cast<uint2*>(scratch(ctx, S_HSUM, n * sizeof(uint2)));
         int* queue = static_cast<int*>(scratch(ctx, S_TMP1, (n + 1) * sizeof(int)));
+        uint32_t* runs = static_cast<uint32_t*>(scratch(ctx, S_RUNS, n * sizeof(uint32_t)));
         const int rows = 1;
         dim3 b(128, rows);
         dim3 g((w + 127) / 128, h);
-        const size_t hsm = static_cast<size_t>(kSlowWarps) * cap * sizeof(unsigned short);
+        const size_t hsm = static_cast<size_t>(kSlowWarps) * (cap / 2) * sizeof(uint32_t);
         smem_attr(ctx, k_ref_slow, static_cast<int>(hsm));
+        const size_t rsm = static_cast<size_t>((w + 31) / 32) * sizeof(uint32_t);
+        smem_attr(ctx, k_ref_runs, static_cast<int>(rsm));
         const float* src = disp;
         for (int it = 0; it < iters; ++it) {
             float* dst = (it == iters - 1) ? out : bufs2[it & 1];
-            k_ref_hminmax<<<g, b, 0, ctx->stream>>>(src, w, h, l, r, cap, mm);
+            k_ref_runs<<<h, 256, rsm, ctx->stream>>>(src, w, h, cap, runs);
+            launched(ctx, "k_ref_runs");
+            k_ref_hminmax<<<g, b, 0, ctx->stream>>>(runs, w, h, l, r, mm);
             launched(ctx, "k_ref_hminmax");
             cuda_check(cudaMemsetAsync(queue, 0, sizeof(int), ctx->stream), "memset");
             k_ref_vminmax<<<g, b, 0, ctx->stream>>>(src, w, h, u, d, mm, dst, queue);
             launched(ctx, "k_ref_vminmax");
-            k_ref_slow<<<sm_count(ctx) * 4, kSlowWarps * 32, hsm, ctx->stream>>>(src, w, h, l, r, u, d, cap, queue,
+            k_ref_slow<<<sm_count(ctx) * 4, kSlowWarps * 32, hsm, ctx->stream>>>(runs, w, h, l, r, u, d, cap, queue,
                                                                                  dst);
             launched(ctx, "k_ref_slow");
             src = dst;
