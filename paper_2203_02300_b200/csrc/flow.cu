@@ -105,12 +105,17 @@ __global__ void k_flow_upsample(const float* __restrict__ cu, const float* __res
 }
 
 // search_patch, flow.cpp:72-121, one WARP per patch; z = direction. Lanes
-// own samples n = lane and lane + 32 (the 64 bilinear samples of an
-// iteration run in parallel); every product gx*r, gy*r, r*r of two floats is
-// exact in double, so the reference's sequential sums are reproduced by
-// lanes 0, 1, 2 adding the exact terms in (dy, dx) order -- the same three
-// rounding chains, run side by side.
+// own samples n = lane and lane + 32 (template and gradients stay in their
+// registers); every product gx*r, gy*r, r*r of two floats is exact in double,
+// so the reference's sequential sums are reproduced by one lane per sum adding
+// the exact terms in (dy, dx) order -- the same rounding chains, run side by
+// side. The Hessian's three chains and the first iteration's three (whose
+// samples need only the seed) run together on lanes 0..5: most patches
+// converge in that first iteration, so a patch typically costs one chain
+// phase instead of two. Term rows are 65 doubles apart: the chain lanes' loads
+// fall in distinct bank pairs.
 constexpr int kPatchWarps = 4;
+constexpr int kTermPitch = 65;
 
 __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* __restrict__ from,
                                                                   const float* __restrict__ to0,
@@ -121,10 +126,7 @@ __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* 
                                                                   size_t field_stride, float* __restrict__ res_base,
                                                                   size_t res_stride) {
     constexpr int N = kPatch * kPatch;
-    __shared__ float s_t[kPatchWarps][N];
-    __shared__ float s_gx[kPatchWarps][N];
-    __shared__ float s_gy[kPatchWarps][N];
-    __shared__ double s_term[kPatchWarps][3][N];
+    __shared__ double s_term[kPatchWarps][6 * kTermPitch];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int j = blockIdx.x * kPatchWarps + wp;
     if (j >= nx * ny) return;  // warp-uniform
@@ -137,12 +139,11 @@ __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* 
     const int cx = min(px + kPatch / 2, w - 1), cy = min(py + kPatch / 2, h - 1);
     const float seed_u = iu[static_cast<size_t>(cy) * w + cx];
     const float seed_v = iv[static_cast<size_t>(cy) * w + cx];
-    float* t = s_t[wp];
-    float* gxs = s_gx[wp];
-    float* gys = s_gy[wp];
-    double* term = &s_term[wp][0][0];
+    double* term = s_term[wp];
+    float tv[2], gxv[2], gyv[2];
 
-    // template, gradients and the Hessian terms (flow.cpp:78-89)
+    // template, gradients and the Hessian terms (flow.cpp:78-89), and the
+    // first iteration's terms at the seed (flow.cpp:93-100)
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         const int n = lane + 32 * half;
@@ -150,27 +151,33 @@ __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* 
         const int ym = max(y - 1, 0), yp = min(y + 1, h - 1);
         const int xm = max(x - 1, 0), xp = min(x + 1, w - 1);
         const float* row = from + static_cast<size_t>(y) * w;
-        const float tv = __ldg(row + x);
-        const float gx = 0.5f * (__ldg(row + xp) - __ldg(row + xm));
-        const float gy =
+        tv[half] = __ldg(row + x);
+        gxv[half] = 0.5f * (__ldg(row + xp) - __ldg(row + xm));
+        gyv[half] =
             0.5f * (__ldg(from + static_cast<size_t>(yp) * w + x) - __ldg(from + static_cast<size_t>(ym) * w + x));
-        t[n] = tv;
-        gxs[n] = gx;
-        gys[n] = gy;
-        term[0 * N + n] = static_cast<double>(gx) * gx;
-        term[1 * N + n] = static_cast<double>(gx) * gy;
-        term[2 * N + n] = static_cast<double>(gy) * gy;
+        const float r = sample_bilinear(to, w, h, static_cast<float>(x) + seed_u, static_cast<float>(y) + seed_v) -
+                        tv[half];
+        term[0 * kTermPitch + n] = static_cast<double>(gxv[half]) * gxv[half];
+        term[1 * kTermPitch + n] = static_cast<double>(gxv[half]) * gyv[half];
+        term[2 * kTermPitch + n] = static_cast<double>(gyv[half]) * gyv[half];
+        term[3 * kTermPitch + n] = static_cast<double>(gxv[half]) * r;
+        term[4 * kTermPitch + n] = static_cast<double>(gyv[half]) * r;
+        term[5 * kTermPitch + n] = static_cast<double>(r) * r;
     }
     __syncwarp();
-    double acc = (lane == 1) ? 0.0 : 1e-6;  // h00, h01, h11 on lanes 0, 1, 2
-    if (lane < 3) {
-        const double* tl = term + lane * N;
+    // h00, h01, h11 (from 1e-6, 0, 1e-6) on lanes 0..2; bu, bv, sse on 3..5
+    double acc = (lane == 0 || lane == 2) ? 1e-6 : 0.0;
+    if (lane < 6) {
+        const double* tl = term + lane * kTermPitch;
 #pragma unroll 16
         for (int n = 0; n < N; ++n) acc += tl[n];
     }
     const double h00 = __shfl_sync(0xffffffffu, acc, 0);
     const double h01 = __shfl_sync(0xffffffffu, acc, 1);
     const double h11 = __shfl_sync(0xffffffffu, acc, 2);
+    double bu = __shfl_sync(0xffffffffu, acc, 3);
+    double bv = __shfl_sync(0xffffffffu, acc, 4);
+    double sse = __shfl_sync(0xffffffffu, acc, 5);
     const double det = h00 * h11 - h01 * h01;
     const double inv00 = h11 / det, inv01 = -h01 / det, inv11 = h00 / det;
 
@@ -178,27 +185,29 @@ __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* 
     double mse = 0.0;
     const float fw = static_cast<float>(w), fh = static_cast<float>(h);
     for (int iter = 0; iter < kIters; ++iter) {
-        __syncwarp();  // previous iteration's term reads are done
+        if (iter > 0) {
+            __syncwarp();  // previous iteration's term reads are done
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int n = lane + 32 * half;
-            const float sx = static_cast<float>(px + (n & 7)) + u;
-            const float sy = static_cast<float>(py + (n >> 3)) + v;
-            const float r = sample_bilinear(to, w, h, sx, sy) - t[n];
-            term[0 * N + n] = static_cast<double>(gxs[n]) * r;
-            term[1 * N + n] = static_cast<double>(gys[n]) * r;
-            term[2 * N + n] = static_cast<double>(r) * r;
-        }
-        __syncwarp();
-        double sum = 0.0;  // bu, bv, sse on lanes 0, 1, 2
-        if (lane < 3) {
-            const double* tl = term + lane * N;
+            for (int half = 0; half < 2; ++half) {
+                const int n = lane + 32 * half;
+                const float sx = static_cast<float>(px + (n & 7)) + u;
+                const float sy = static_cast<float>(py + (n >> 3)) + v;
+                const float r = sample_bilinear(to, w, h, sx, sy) - tv[half];
+                term[0 * kTermPitch + n] = static_cast<double>(gxv[half]) * r;
+                term[1 * kTermPitch + n] = static_cast<double>(gyv[half]) * r;
+                term[2 * kTermPitch + n] = static_cast<double>(r) * r;
+            }
+            __syncwarp();
+            double sum = 0.0;  // bu, bv, sse on lanes 0, 1, 2
+            if (lane < 3) {
+                const double* tl = term + lane * kTermPitch;
 #pragma unroll 16
-            for (int n = 0; n < N; ++n) sum += tl[n];
+                for (int n = 0; n < N; ++n) sum += tl[n];
+            }
+            bu = __shfl_sync(0xffffffffu, sum, 0);
+            bv = __shfl_sync(0xffffffffu, sum, 1);
+            sse = __shfl_sync(0xffffffffu, sum, 2);
         }
-        const double bu = __shfl_sync(0xffffffffu, sum, 0);
-        const double bv = __shfl_sync(0xffffffffu, sum, 1);
-        const double sse = __shfl_sync(0xffffffffu, sum, 2);
         mse = sse / (kPatch * kPatch);
         const double step_u = inv00 * bu + inv01 * bv;
         const double step_v = inv01 * bu + inv11 * bv;

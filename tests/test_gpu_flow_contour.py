@@ -189,3 +189,19 @@ def test_flow_ragged_shapes(gpu, ref, w, h):
     u, v = ref.compute_flow(a, b, cfg)
     gu, gv = gpu.compute_flow(T(a), T(b), cfg)
     assert bits_equal(N(gu), u) and bits_equal(N(gv), v)
+
+
+def test_flow_nonfinite_and_pinned(gpu, ref):
+    """k_flow_patch_w against the reference: a textured pair with a NaN blob
+    in the target (non-finite steps in the merged first chain phase and in
+    later iterations: seed restored, zero-weight patches, the nearest-covered
+    fill) and a ragged size with pinned last patches."""
+    cfg = Config()
+    for w, h, blob in ((160, 96, True), (203, 77, False)):
+        a = random_image(w, h, 5 * w + h)
+        b = np.roll(a, (2, -3), axis=(0, 1)).astype(np.float32)
+        if blob:
+            b[40:52, 60:75] = np.nan
+        u, v = ref.compute_flow(a, b, cfg)
+        gu, gv = gpu.compute_flow(T(a), T(b), cfg)
+        assert bits_equal(N(gu), u) and bits_equal(N(gv), v), (w, h)
