@@ -78,12 +78,13 @@ void smem_attr(dco_ctx* ctx, const void* fn, int bytes, bool carveout) {
     static std::mutex mu;
     static std::map<std::pair<int, const void*>, int> done;
     std::lock_guard<std::mutex> lock(mu);
-    int& have = done[{ctx->device, fn}];
-    if (have >= bytes) return;
-    cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attr");
+    int& have = done[{ctx->device, fn}];  // bytes + 1 once set (0 = never)
+    if (have > bytes) return;
+    if (bytes > 0)
+        cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attr");
     if (carveout)
         cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
-    have = bytes;
+    have = bytes + 1;
 }
 
 int sm_count(dco_ctx* ctx) {

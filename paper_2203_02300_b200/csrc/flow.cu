@@ -104,16 +104,18 @@ __global__ void k_flow_upsample(const float* __restrict__ cu, const float* __res
     fv[o] = 2.0f * (tv * (1 - fy) + bv * fy);
 }
 
-// search_patch, flow.cpp:72-121, one WARP per patch; z = direction. Lanes
-// own samples n = lane and lane + 32 (template and gradients stay in their
-// registers); every product gx*r, gy*r, r*r of two floats is exact in double,
-// so the reference's sequential sums are reproduced by one lane per sum adding
-// the exact terms in (dy, dx) order -- the same rounding chains, run side by
-// side. The Hessian's three chains and the first iteration's three (whose
-// samples need only the seed) run together on lanes 0..5: most patches
-// converge in that first iteration, so a patch typically costs one chain
-// phase instead of two. Term rows are 65 doubles apart: the chain lanes' loads
-// fall in distinct bank pairs.
+// search_patch, flow.cpp:72-121, one HALF-WARP per patch (two patches per
+// warp); z = direction. Lane l of a half owns samples n = l + 16 q, q < 4
+// (template and gradients stay in its registers); every product gx*r, gy*r,
+// r*r of two floats is exact in double, so the reference's sequential sums
+// are reproduced by one lane per sum adding the exact terms in (dy, dx)
+// order -- the same rounding chains, run side by side (both halves' chains
+// share each instruction, as do the divisions and the step). The Hessian's
+// three chains and the first iteration's three (whose samples need only the
+// seed) run together on lanes 0..5 of the half: most patches converge in that
+// first iteration. A half whose patch is done idles until the other's is.
+// Term rows are 65 doubles apart: the chain lanes' loads fall in distinct
+// bank pairs.
 constexpr int kPatchWarps = 4;
 constexpr int kTermPitch = 65;
 
@@ -126,10 +128,14 @@ __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* 
                                                                   size_t field_stride, float* __restrict__ res_base,
                                                                   size_t res_stride) {
     constexpr int N = kPatch * kPatch;
-    __shared__ double s_term[kPatchWarps][6 * kTermPitch];
+    __shared__ double s_term[kPatchWarps][2][6 * kTermPitch];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    const int j = blockIdx.x * kPatchWarps + wp;
-    if (j >= nx * ny) return;  // warp-uniform
+    const int hl = lane >> 4, ll = lane & 15;
+    const int j0 = (blockIdx.x * kPatchWarps + wp) * 2;
+    const int np = nx * ny;
+    if (j0 >= np) return;  // warp-uniform
+    const int j = min(j0 + hl, np - 1);  // an odd last patch: the second half repeats it, inactive
+    bool active = j0 + hl < np;
     const float* to = blockIdx.z ? to1 : to0;
     const float* iu = init_u_base + blockIdx.z * field_stride;
     const float* iv = init_v_base + blockIdx.z * field_stride;
@@ -139,75 +145,78 @@ __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* 
     const int cx = min(px + kPatch / 2, w - 1), cy = min(py + kPatch / 2, h - 1);
     const float seed_u = iu[static_cast<size_t>(cy) * w + cx];
     const float seed_v = iv[static_cast<size_t>(cy) * w + cx];
-    double* term = s_term[wp];
-    float tv[2], gxv[2], gyv[2];
+    double* term = s_term[wp][hl];
+    float tv[4], gxv[4], gyv[4];
 
     // template, gradients and the Hessian terms (flow.cpp:78-89), and the
     // first iteration's terms at the seed (flow.cpp:93-100)
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-        const int n = lane + 32 * half;
+    for (int q = 0; q < 4; ++q) {
+        const int n = ll + 16 * q;
         const int y = py + (n >> 3), x = px + (n & 7);
         const int ym = max(y - 1, 0), yp = min(y + 1, h - 1);
         const int xm = max(x - 1, 0), xp = min(x + 1, w - 1);
         const float* row = from + static_cast<size_t>(y) * w;
-        tv[half] = __ldg(row + x);
-        gxv[half] = 0.5f * (__ldg(row + xp) - __ldg(row + xm));
-        gyv[half] =
-            0.5f * (__ldg(from + static_cast<size_t>(yp) * w + x) - __ldg(from + static_cast<size_t>(ym) * w + x));
-        const float r = sample_bilinear(to, w, h, static_cast<float>(x) + seed_u, static_cast<float>(y) + seed_v) -
-                        tv[half];
-        term[0 * kTermPitch + n] = static_cast<double>(gxv[half]) * gxv[half];
-        term[1 * kTermPitch + n] = static_cast<double>(gxv[half]) * gyv[half];
-        term[2 * kTermPitch + n] = static_cast<double>(gyv[half]) * gyv[half];
-        term[3 * kTermPitch + n] = static_cast<double>(gxv[half]) * r;
-        term[4 * kTermPitch + n] = static_cast<double>(gyv[half]) * r;
+        tv[q] = __ldg(row + x);
+        gxv[q] = 0.5f * (__ldg(row + xp) - __ldg(row + xm));
+        gyv[q] = 0.5f * (__ldg(from + static_cast<size_t>(yp) * w + x) - __ldg(from + static_cast<size_t>(ym) * w + x));
+        const float r =
+            sample_bilinear(to, w, h, static_cast<float>(x) + seed_u, static_cast<float>(y) + seed_v) - tv[q];
+        term[0 * kTermPitch + n] = static_cast<double>(gxv[q]) * gxv[q];
+        term[1 * kTermPitch + n] = static_cast<double>(gxv[q]) * gyv[q];
+        term[2 * kTermPitch + n] = static_cast<double>(gyv[q]) * gyv[q];
+        term[3 * kTermPitch + n] = static_cast<double>(gxv[q]) * r;
+        term[4 * kTermPitch + n] = static_cast<double>(gyv[q]) * r;
         term[5 * kTermPitch + n] = static_cast<double>(r) * r;
     }
     __syncwarp();
-    // h00, h01, h11 (from 1e-6, 0, 1e-6) on lanes 0..2; bu, bv, sse on 3..5
-    double acc = (lane == 0 || lane == 2) ? 1e-6 : 0.0;
-    if (lane < 6) {
-        const double* tl = term + lane * kTermPitch;
+    // h00, h01, h11 (from 1e-6, 0, 1e-6) on lanes 0..2 of the half; bu, bv, sse on 3..5
+    double acc = (ll == 0 || ll == 2) ? 1e-6 : 0.0;
+    if (ll < 6) {
+        const double* tl = term + ll * kTermPitch;
 #pragma unroll 16
         for (int n = 0; n < N; ++n) acc += tl[n];
     }
-    const double h00 = __shfl_sync(0xffffffffu, acc, 0);
-    const double h01 = __shfl_sync(0xffffffffu, acc, 1);
-    const double h11 = __shfl_sync(0xffffffffu, acc, 2);
-    double bu = __shfl_sync(0xffffffffu, acc, 3);
-    double bv = __shfl_sync(0xffffffffu, acc, 4);
-    double sse = __shfl_sync(0xffffffffu, acc, 5);
+    const int hb = lane & 16;  // the half's lane 0
+    const double h00 = __shfl_sync(0xffffffffu, acc, hb + 0);
+    const double h01 = __shfl_sync(0xffffffffu, acc, hb + 1);
+    const double h11 = __shfl_sync(0xffffffffu, acc, hb + 2);
+    double bu = __shfl_sync(0xffffffffu, acc, hb + 3);
+    double bv = __shfl_sync(0xffffffffu, acc, hb + 4);
+    double sse = __shfl_sync(0xffffffffu, acc, hb + 5);
     const double det = h00 * h11 - h01 * h01;
     const double inv00 = h11 / det, inv01 = -h01 / det, inv11 = h00 / det;
 
     float u = seed_u, v = seed_v;
     double mse = 0.0;
     const float fw = static_cast<float>(w), fh = static_cast<float>(h);
-    for (int iter = 0; iter < kIters; ++iter) {
+    for (int iter = 0; iter < kIters && __any_sync(0xffffffffu, active); ++iter) {
         if (iter > 0) {
             __syncwarp();  // previous iteration's term reads are done
+            if (active) {
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const int n = lane + 32 * half;
-                const float sx = static_cast<float>(px + (n & 7)) + u;
-                const float sy = static_cast<float>(py + (n >> 3)) + v;
-                const float r = sample_bilinear(to, w, h, sx, sy) - tv[half];
-                term[0 * kTermPitch + n] = static_cast<double>(gxv[half]) * r;
-                term[1 * kTermPitch + n] = static_cast<double>(gyv[half]) * r;
-                term[2 * kTermPitch + n] = static_cast<double>(r) * r;
+                for (int q = 0; q < 4; ++q) {
+                    const int n = ll + 16 * q;
+                    const float sx = static_cast<float>(px + (n & 7)) + u;
+                    const float sy = static_cast<float>(py + (n >> 3)) + v;
+                    const float r = sample_bilinear(to, w, h, sx, sy) - tv[q];
+                    term[0 * kTermPitch + n] = static_cast<double>(gxv[q]) * r;
+                    term[1 * kTermPitch + n] = static_cast<double>(gyv[q]) * r;
+                    term[2 * kTermPitch + n] = static_cast<double>(r) * r;
+                }
             }
             __syncwarp();
-            double sum = 0.0;  // bu, bv, sse on lanes 0, 1, 2
-            if (lane < 3) {
-                const double* tl = term + lane * kTermPitch;
+            double sum = 0.0;  // bu, bv, sse on lanes 0, 1, 2 of the half
+            if (ll < 3 && active) {
+                const double* tl = term + ll * kTermPitch;
 #pragma unroll 16
                 for (int n = 0; n < N; ++n) sum += tl[n];
             }
-            bu = __shfl_sync(0xffffffffu, sum, 0);
-            bv = __shfl_sync(0xffffffffu, sum, 1);
-            sse = __shfl_sync(0xffffffffu, sum, 2);
+            bu = __shfl_sync(0xffffffffu, sum, hb + 0);
+            bv = __shfl_sync(0xffffffffu, sum, hb + 1);
+            sse = __shfl_sync(0xffffffffu, sum, hb + 2);
         }
+        if (!active) continue;
         mse = sse / (kPatch * kPatch);
         const double step_u = inv00 * bu + inv01 * bv;
         const double step_v = inv01 * bu + inv11 * bv;
@@ -216,13 +225,14 @@ __global__ void __launch_bounds__(kPatchWarps * 32) k_flow_patch_w(const float* 
         if (!isfinite(u) || !isfinite(v)) {
             u = seed_u;
             v = seed_v;
-            break;
+            active = false;
+            continue;
         }
         u = clampf(u, -fw, fw);
         v = clampf(v, -fh, fh);
-        if (step_u * step_u + step_v * step_v < 1e-6) break;
+        if (step_u * step_u + step_v * step_v < 1e-6) active = false;
     }
-    if (lane == 0) {
+    if (ll == 0 && j0 + hl < np) {
         res[3 * j + 0] = u;
         res[3 * j + 1] = v;
         res[3 * j + 2] = static_cast<float>(1.0 / (mse + 1e-2));
@@ -376,6 +386,7 @@ void compute_flow_multi(dco_ctx* ctx, const float* from, const float* const* to,
     auto V = [&](int buf, int k) { return fld + buf * 4 * max_level + k * fs + max_level; };
     int cur = 0;
     cuda_check(cudaMemsetAsync(fld, 0, max_level * 8 * sizeof(float), ctx->stream), "memset");
+    smem_attr(ctx, k_flow_patch_w, 0, true);  // the whole carveout: 26 KB blocks, register-limited
     dim3 b(32, 8);
     for (int l = levels - 1; l >= 0; --l) {
         const Level& L = lv[l];
@@ -387,7 +398,8 @@ void compute_flow_multi(dco_ctx* ctx, const float* from, const float* const* to,
             cur ^= 1;
         }
         int np = L.nx * L.ny;
-        k_flow_patch_w<<<dim3((np + kPatchWarps - 1) / kPatchWarps, 1, dirs), kPatchWarps * 32, 0, ctx->stream>>>(
+        const int npw = (np + 1) / 2;  // warps: two patches each
+        k_flow_patch_w<<<dim3((npw + kPatchWarps - 1) / kPatchWarps, 1, dirs), kPatchWarps * 32, 0, ctx->stream>>>(
             p_from[l], p_to[0][l], dirs > 1 ? p_to[1][l] : p_to[0][l], L.w, L.h, L.nx, L.ny, U(cur, 0), V(cur, 0), fs, res,
             max_patches * 3);
         launched(ctx, "k_flow_patch_w");
