@@ -42,7 +42,7 @@ sys.path.insert(0, ROOT)
 W, H, D = 1280, 720, 128
 NQ, NF = (W // 2) * (H // 2), W * H
 METRIC = "stereo frames/sec at 1280x720 D=128 (1/2/4/8 B200) vs CPU; HBM GB/s fraction"
-STREAMS_PER_GPU = 6
+STREAMS_PER_GPU = 8
 # the workload, identical in both arms' lines (arm-specific details go under "arm")
 CONFIG = {
     "workload": "DCO frame 1280x720 D=128 steady state (stereo+flow+contour+densify+render+composite)",
@@ -50,7 +50,7 @@ CONFIG = {
     "frames": "synthetic stereo video (paper_2203_02300_b200.synth), independent streams, d_pre chain active",
     "virtual_layer": "cube mesh (0.3 m) rendered per frame under a per-frame pose",
     "l2": "GPU arm: flushed (160 MiB memset, L2 is 126 MB) before every frame, inside the timed region",
-    "parallelism": "frames shard as independent streams: 6 per GPU x N GPUs (GPU arm), one per host core "
+    "parallelism": "frames shard as independent streams: 8 per GPU x N GPUs (GPU arm), one per host core "
                    "(reference arm); no data-path collective",
 }
 
@@ -585,7 +585,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=6, help="concurrent pipeline streams per GPU")
+    ap.add_argument("--streams", type=int, default=STREAMS_PER_GPU, help="concurrent pipeline streams per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
