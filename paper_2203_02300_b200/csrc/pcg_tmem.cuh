@@ -104,10 +104,16 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
     double* s_cv = sx + 2 * w + 2 * chunk + t;
     double* s_pr = sx + 2 * w + 3 * chunk + t;
     // shared-window byte addresses of this thread's slot 0 (loop accesses)
-    const uint32_t aP = static_cast<uint32_t>(__cvta_generic_to_shared(s_p));
-    const uint32_t aCH = static_cast<uint32_t>(__cvta_generic_to_shared(s_ch));
-    const uint32_t aCV = static_cast<uint32_t>(__cvta_generic_to_shared(s_cv));
-    const uint32_t aPR = static_cast<uint32_t>(__cvta_generic_to_shared(s_pr));
+    // opaque to the compiler: kept (or spilled) rather than rebuilt from the
+    // shared-window base at every use
+    auto opaque = [](uint32_t v) {
+        asm volatile("" : "+r"(v));
+        return v;
+    };
+    const uint32_t aP = opaque(static_cast<uint32_t>(__cvta_generic_to_shared(s_p)));
+    const uint32_t aCH = opaque(static_cast<uint32_t>(__cvta_generic_to_shared(s_ch)));
+    const uint32_t aCV = opaque(static_cast<uint32_t>(__cvta_generic_to_shared(s_cv)));
+    const uint32_t aPR = opaque(static_cast<uint32_t>(__cvta_generic_to_shared(s_pr)));
     const uint32_t wb = 8u * static_cast<uint32_t>(w);
     unsigned gen = 0;
     double r[EPT], x[EPT];
