@@ -706,7 +706,7 @@ namespace {
 inline dim3 grid2(int w, int h, dim3 b) { return dim3((w + b.x - 1) / b.x, (h + b.y - 1) / b.y); }
 
 long long* g_pcg_dbg = nullptr;
-constexpr int kDbgLen = 1280 + 64 * 1024 * 3;  // + per-block globaltimer stamps
+constexpr int kDbgLen = 1280 + 64 * 1024 * 3 + 1024;  // + per-block globaltimer stamps, per-block SM ids
 
 // "k_pcg_tmem<7>"-style instance names with stable storage (dco_last_solver)
 const char* instance_name(const char* base, int ept) {

@@ -126,6 +126,11 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
         a.dbg[636] = static_cast<long long>(gt_);
     }
+    if (a.dbg && t == 0) {  // this block's SM (DCO_PCG_DEBUG)
+        unsigned smid_;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+        a.dbg[1280 + 64 * 1024 * 3 + blockIdx.x] = smid_;
+    }
     unsigned long long anchors = a.anchors_dev ? *a.anchors_dev : a.anchors_host;
     if (anchors == 0) {
         const float* fb = (a.fallback && (!a.fallback_valid || *a.fallback_valid)) ? a.fallback : nullptr;

@@ -22,10 +22,10 @@ for i in range(4):
 torch.cuda.synchronize()
 lib = native.load()
 NB = torch.cuda.get_device_properties(0).multi_processor_count
-LEN = 1280 + 64 * 1024 * 3
+LEN = 1280 + 64 * 1024 * 3 + 1024
 buf = (ctypes.c_longlong * LEN)()
 lib.dco_debug_pcg_stamps(buf, LEN)
-g = np.array(buf[1280:]).reshape(64, 1024, 3)[:, :NB, :].astype(np.float64)
+g = np.array(buf[1280:1280 + 64 * 1024 * 3]).reshape(64, 1024, 3)[:, :NB, :].astype(np.float64)
 a = np.array(buf[:640]).reshape(64, 10)
 b = np.array(buf[640:1280]).reshape(64, 10)
 # stamps: 0 loop head, 3 after halo, 4 after P1, 5 after CTA barrier, 1 after P2, 2 after grid barrier
@@ -53,6 +53,12 @@ wm = work.mean(0)
 order = np.argsort(-wm)
 print("slowest blocks:", [(int(b), int(wm[b])) for b in order[:8]])
 print("fastest blocks:", [(int(b), int(wm[b])) for b in order[-4:]])
+smid = np.array(buf[1280 + 64 * 1024 * 3:1280 + 64 * 1024 * 3 + NB])
+print("SM ids of the slowest blocks:", [int(smid[b]) for b in order[:12]])
+print("SM ids of the fastest blocks:", [int(smid[b]) for b in order[-12:]])
+print("SM ids by block:", [int(v) for v in smid])
+halo_ns = (g[it, :, 0] - g[4:39, :, 2])  # loop head after the previous release: the scalar math
+print("per-block work ns (block order):", [int(v) for v in wm])
 # block 0 globaltimer (ns): kernel entry (after the anchor check), after the
 # setup barrier, loop exit, after the final objective barrier
 e = np.array(buf[6:10], dtype=np.float64)
