@@ -423,22 +423,35 @@ def run_ours(args, world, rank, local):
     outs = [(torch.empty((H, W, 3)).pin_memory(), torch.empty((H, W), dtype=torch.uint8).pin_memory(),
              torch.empty((H, W)).pin_memory()) for _ in range(S)]
 
-    def e2e_worker(s, n):
-        for _ in range(n):
+    # S x K frames in total, handed out one at a time: a thread whose stream
+    # runs ahead takes the next frame of its own stream (each stream's frames
+    # stay in order, d_pre chained), so the run does not end on a tail of
+    # stragglers while the other threads idle
+    tickets = [0]
+    lock = th.Lock()
+
+    def e2e_worker(s):
+        while True:
+            with lock:
+                if tickets[0] <= 0:
+                    return
+                tickets[0] -= 1
             k = pos[s] % nframes
             streams[s].set_next_pose(frame_pose(pos[s]))
             streams[s].push_gray8_host(hl[s][k], hr[s][k], *outs[s])
             pos[s] += 1
 
-    ths = [th.Thread(target=e2e_worker, args=(s, 2)) for s in range(S)]
-    [t.start() for t in ths]
-    [t.join() for t in ths]
+    def e2e_run(total):
+        tickets[0] = total
+        ths = [th.Thread(target=e2e_worker, args=(s,)) for s in range(S)]
+        [t.start() for t in ths]
+        [t.join() for t in ths]
+
+    e2e_run(2 * S)
     barrier()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
-    ths = [th.Thread(target=e2e_worker, args=(s, args.steps)) for s in range(S)]
-    [t.start() for t in ths]
-    [t.join() for t in ths]
+    e2e_run(args.steps * S)
     e2e_total = 1000.0 * (time.perf_counter() - w0)
     barrier()
 
