@@ -420,7 +420,9 @@ def run_ours(args, world, rank, local):
     # dense out, S host threads (ctypes releases the GIL) driving S contexts
     hl = [[torch.from_numpy(f[0]).pin_memory() for f in h] for h in host]
     hr = [[torch.from_numpy(f[1]).pin_memory() for f in h] for h in host]
-    outs = [(torch.empty((H, W, 3)).pin_memory(), torch.empty((H, W), dtype=torch.uint8).pin_memory(),
+    # the frame's outputs as run_pipeline writes them (pipeline.cpp:266-268):
+    # composite RGB bytes, mask bytes, dense floats
+    outs = [(torch.empty((H, W, 3), dtype=torch.uint8).pin_memory(), torch.empty((H, W), dtype=torch.uint8).pin_memory(),
              torch.empty((H, W)).pin_memory()) for _ in range(S)]
 
     # S x K frames in total, handed out one at a time: a thread whose stream
@@ -438,7 +440,7 @@ def run_ours(args, world, rank, local):
                 tickets[0] -= 1
             k = pos[s] % nframes
             streams[s].set_next_pose(frame_pose(pos[s]))
-            streams[s].push_gray8_host(hl[s][k], hr[s][k], *outs[s])
+            streams[s].push_gray8_host_encoded(hl[s][k], hr[s][k], *outs[s])
             pos[s] += 1
 
     def e2e_run(total):
@@ -502,8 +504,10 @@ def run_ours(args, world, rank, local):
         "frame_ms_isolated": round(sum(per_frame.values()), 4),
         "densify_iterations": iters,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": 2 * NF * S * world,
-                "d2h_bytes_per_step": (NF * 3 * 4 + NF + NF * 4) * S * world,
-                "path": "dco_stream_push_gray8_host (pinned host u8 in; composite, mask, dense out)"},
+                "d2h_bytes_per_step": (NF * 3 + NF + NF * 4) * S * world,
+                "path": "dco_stream_push_gray8_host_encoded (pinned host u8 in; out: the frame's files' contents "
+                        "as run_pipeline writes them, pipeline.cpp:266-268 -- composite RGB bytes (write_ppm), "
+                        "mask bytes (write_mask_pgm), dense floats (write_pfm))"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

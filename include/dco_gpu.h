@@ -302,6 +302,15 @@ int dco_stream_push_f32(dco_stream* s, const float* left, const float* right, co
 int dco_stream_push_gray8_host(dco_stream* s, const uint8_t* left8, const uint8_t* right8,
                                float* composite_out, uint8_t* mask_out, float* dense_out,
                                dco_frame_result* result);
+/* Host-buffer variant with the frame's outputs in the encodings run_pipeline
+ * writes them (pipeline.cpp:266-268): the composite as write_ppm's 8-bit RGB
+ * bytes (quantize, codec.cpp:23-26 and 221-229; 3*w*h bytes), the mask as
+ * write_mask_pgm's bytes (0 / 255, codec.cpp:243-247; w*h), the dense map as
+ * the floats write_pfm stores (w*h). Quantised on the device, so 7.4 MB per
+ * 1280x720 frame cross PCIe instead of 15.7 MB. Any output may be NULL. */
+int dco_stream_push_gray8_host_encoded(dco_stream* s, const uint8_t* left8, const uint8_t* right8,
+                                       uint8_t* composite_rgb8, uint8_t* mask8, float* dense_out,
+                                       dco_frame_result* result);
 int dco_stream_views(const dco_stream* s, dco_frame_views* views);
 
 /* Per-span CUDA-event timing of composited frames: the device-side

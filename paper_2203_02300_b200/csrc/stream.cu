@@ -156,6 +156,22 @@ __global__ void k_rgb_from_f32(const float* __restrict__ gray, const float* __re
 }
 
 // previous_dense = dense when the solve succeeded (pipeline.cpp:235).
+// The frame's outputs in run_pipeline's file encodings (pipeline.cpp:266-267):
+// the composite as write_ppm's bytes (quantize, codec.cpp:23-26, 221-229) and
+// the mask as write_mask_pgm's (0 / 255, codec.cpp:243-247). Thread per pixel.
+__global__ void k_encode_frame(const float* __restrict__ comp, const uint8_t* __restrict__ mask, size_t n,
+                               uint8_t* __restrict__ rgb8, uint8_t* __restrict__ mask8) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        float v = comp[3 * i + c];
+        v = v < 0.0f ? 0.0f : (1.0f < v ? 1.0f : v);  // std::clamp: NaN passes through
+        rgb8[3 * i + c] = isnan(v) ? 0 : static_cast<uint8_t>(lroundf(v * 255.0f));
+    }
+    mask8[i] = mask[i] ? 255 : 0;
+}
+
 __global__ void k_keep_dense(const float* __restrict__ dense, size_t n, const int* __restrict__ status,
                              float* __restrict__ prev, int* __restrict__ prev_valid) {
     if (*status != 0) return;
@@ -236,6 +252,7 @@ struct dco_stream {
     double next_pose[16] = {};
     bool next_pose_set = false;
     void* host_out = nullptr;
+    uint8_t* enc = nullptr;  // encoded outputs (4 bytes per pixel), allocated on first use
     // optional per-span CUDA-event timing (StageTimings, pipeline.hpp:27-46)
     // A ring of kRing event sets so the host never waits on the frame it just
     // enqueued: set i is harvested when it is about to be reused (or flushed).
@@ -641,6 +658,43 @@ int dco_stream_push_gray8_host(dco_stream* s, const uint8_t* left8, const uint8_
                 cuda_check(cudaMemcpyAsync(comp_out, s->comp, 3 * nf * 4, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
             if (mask_out)
                 cuda_check(cudaMemcpyAsync(mask_out, s->mask, nf, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+            if (dense_out)
+                cuda_check(cudaMemcpyAsync(dense_out, s->dense, nf * 4, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+        }
+        cuda_check(cudaStreamSynchronize(ctx->stream), "sync");
+    });
+}
+
+int dco_stream_push_gray8_host_encoded(dco_stream* s, const uint8_t* left8, const uint8_t* right8,
+                                       uint8_t* composite_rgb8, uint8_t* mask8, float* dense_out,
+                                       dco_frame_result* res) {
+    if (!s) return DCO_INPUT;
+    return guarded(s->ctx, [&] {
+        dco_ctx* ctx = s->ctx;
+        size_t nf = static_cast<size_t>(s->fw) * s->fh;
+        if (!s->enc) s->enc = s->alloc<uint8_t>(4 * nf);
+        uint8_t* staging = static_cast<uint8_t*>(scratch(ctx, S_STAGE, 2 * nf));
+        cuda_check(cudaMemcpyAsync(staging, left8, nf, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+        cuda_check(cudaMemcpyAsync(staging + nf, right8, nf, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+        if (s->pushed + 1 >= 3) s->begin_frame();
+        int slot = static_cast<int>(s->pushed % 3);
+        s->take_pose(slot);
+        ingest_gray8(ctx, staging, s->fw, s->fh, s->gray[slot], s->left_q[slot]);
+        ingest_gray8(ctx, staging + nf, s->fw, s->fh, nullptr, s->right_q[slot]);
+        k_rgb_from_u8<<<blocks_for(nf, 256), 256, 0, ctx->stream>>>(staging, nullptr, nf, s->rgb[slot]);
+        launched(ctx, "k_rgb_from_u8");
+        finish_push(s, res);
+        if (s->pushed >= 3) {
+            if (composite_rgb8 || mask8) {
+                k_encode_frame<<<blocks_for(nf, 256), 256, 0, ctx->stream>>>(s->comp, s->mask, nf, s->enc,
+                                                                              s->enc + 3 * nf);
+                launched(ctx, "k_encode_frame");
+            }
+            if (composite_rgb8)
+                cuda_check(cudaMemcpyAsync(composite_rgb8, s->enc, 3 * nf, cudaMemcpyDeviceToHost, ctx->stream),
+                           "d2h");
+            if (mask8)
+                cuda_check(cudaMemcpyAsync(mask8, s->enc + 3 * nf, nf, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
             if (dense_out)
                 cuda_check(cudaMemcpyAsync(dense_out, s->dense, nf * 4, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
         }

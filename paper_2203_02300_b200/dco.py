@@ -812,6 +812,20 @@ class Stream:
             self.handle, hp(left8), hp(right8), hp(comp_out), hp(mask_out), hp(dense_out), ctypes.byref(res)))
         return res
 
+    def push_gray8_host_encoded(self, left8, right8, comp_rgb8=None, mask8=None, dense_out=None):
+        """Host buffers in and out, the outputs encoded as run_pipeline writes
+        them (pipeline.cpp:266-268): composite RGB bytes (write_ppm's quantize),
+        mask bytes 0/255 (write_mask_pgm), dense floats."""
+        self._bind()
+        res = native.FrameResult()
+
+        def hp(a):
+            return None if a is None else ctypes.c_void_p(a.ctypes.data if hasattr(a, "ctypes") else a.data_ptr())
+
+        native.check(self.ctx, self.lib.dco_stream_push_gray8_host_encoded(
+            self.handle, hp(left8), hp(right8), hp(comp_rgb8), hp(mask8), hp(dense_out), ctypes.byref(res)))
+        return res
+
     SPANS = ["ingest", "cross", "cost", "aggregate", "wta", "refine", "sparse", "flow", "fusion", "box",
              "normalize", "blur", "contour", "assemble", "solve", "composite"]
 

@@ -185,6 +185,7 @@ SIGNATURES = {
     ),
     "dco_stream_push_f32": (c_int, [c_void_p, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_push_gray8_host": (c_int, [c_void_p, P, P, P, P, P, ctypes.POINTER(FrameResult)]),
+    "dco_stream_push_gray8_host_encoded": (c_int, [c_void_p, P, P, P, P, P, ctypes.POINTER(FrameResult)]),
     "dco_stream_views": (c_int, [c_void_p, ctypes.POINTER(FrameViews)]),
     "dco_stream_set_lr_check": (c_int, [c_void_p, c_int, c_double]),
     "dco_stream_set_timing": (c_int, [c_void_p, c_int]),
