@@ -303,13 +303,20 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
 #pragma unroll
             for (int c = 0; c < 10; ++c) v[c] = 0.0;
             tm_wait_st();  // last phase's q / xs / rs stores have landed
+            // slot k + 1's q, xs, rs (and x) are loaded while slot k computes
+            uint32_t c4[4], c2[2], cx[2] = {0u, 0u};
+            tm_ld4(tm, c4);      // q, xs
+            tm_ld2(tm + 4, c2);  // rs
+            if (XT > 0) tm_ld2(tmx, cx);
+            tm_wait_ld();
             static_for<0, EPT>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                uint32_t c4[4], c2[2], cx[2];
-                tm_ld4(tm + 8 * k, c4);      // q, xs
-                tm_ld2(tm + 8 * k + 4, c2);  // rs
-                if (k < XT) tm_ld2(tmx + 2 * k, cx);
-                tm_wait_ld();
+                uint32_t n4[4], n2[2], nx[2] = {0u, 0u};
+                if constexpr (k + 1 < EPT) {
+                    tm_ld4(tm + 8 * (k + 1), n4);
+                    tm_ld2(tm + 8 * (k + 1) + 4, n2);
+                    if (k + 1 < XT) tm_ld2(tmx + 2 * (k + 1), nx);
+                }
                 const double qk = u2d(c4[0], c4[1]);
                 double xsi = u2d(c4[2], c4[3]);
                 double rsi = u2d(c2[0], c2[1]);
@@ -351,6 +358,15 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
                     d2u(xsi, s4[0], s4[1]);
                     d2u(rsi, s4[2], s4[3]);
                     tm_st4(tm + 8 * k + 2, s4);
+                }
+                if constexpr (k + 1 < EPT) {
+                    tm_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) c4[c] = n4[c];
+                    c2[0] = n2[0];
+                    c2[1] = n2[1];
+                    cx[0] = nx[0];
+                    cx[1] = nx[1];
                 }
             });
             // P1 sums -> per-warp partials in shared memory (frees registers for P2)
