@@ -197,10 +197,14 @@ __global__ void k_census(const float* __restrict__ img, int w, int h, int rw, in
 
 // census_transform over a shared-memory tile (the clamped window of a 32x8
 // block staged once), both images of a stereo pair in one launch (z).
+// RW0 / RH0 > 0: the window's half sizes as compile-time constants (the
+// default 9x7), so the 62 compares unroll into fixed bit positions.
+template <int RW0 = 0, int RH0 = 0>
 __global__ void __launch_bounds__(256) k_census_tiled(const float* __restrict__ img0, const float* __restrict__ img1,
-                                                      int w, int h, int rw, int rh, uint64_t* __restrict__ out0,
+                                                      int w, int h, int rw_, int rh_, uint64_t* __restrict__ out0,
                                                       uint64_t* __restrict__ out1) {
     extern __shared__ float tile[];  // (32 + 2 rw) x (8 + 2 rh)
+    const int rw = RW0 > 0 ? RW0 : rw_, rh = RH0 > 0 ? RH0 : rh_;
     const float* img = blockIdx.z ? img1 : img0;
     uint64_t* out = blockIdx.z ? out1 : out0;
     const int tw = 32 + 2 * rw, th = 8 + 2 * rh;
@@ -216,11 +220,34 @@ __global__ void __launch_bounds__(256) k_census_tiled(const float* __restrict__ 
     const float* c = tile + (threadIdx.y + rh) * tw + threadIdx.x + rw;
     const float center = *c;
     uint64_t bits = 0;
-    for (int dy = -rh; dy <= rh; ++dy) {
-        const float* row = c + dy * tw;
-        for (int dx = -rw; dx <= rw; ++dx) {
-            if (dx == 0 && dy == 0) continue;
-            bits = (bits << 1) | (row[dx] < center ? 1ull : 0ull);
+    if constexpr (RW0 > 0 && RH0 > 0) {
+        // bit of (dy, dx): row-major order, centre skipped, the first compare
+        // ends as the most significant of the (2RW0+1)(2RH0+1)-1 bits
+        constexpr int NB = (2 * RW0 + 1) * (2 * RH0 + 1) - 1;
+        uint32_t hi = 0, lo = 0;  // bits 32..NB-1, bits 0..31
+#pragma unroll
+        for (int dy = -RH0; dy <= RH0; ++dy) {
+#pragma unroll
+            for (int dx = -RW0; dx <= RW0; ++dx) {
+                if (dx == 0 && dy == 0) continue;
+                const int k = (dy + RH0) * (2 * RW0 + 1) + (dx + RW0) - ((dy > 0 || (dy == 0 && dx > 0)) ? 1 : 0);
+                const int pos = NB - 1 - k;
+                const uint32_t b = c[dy * tw + dx] < center ? 1u : 0u;
+                if (pos >= 32) {
+                    hi |= b << (pos - 32);
+                } else {
+                    lo |= b << pos;
+                }
+            }
+        }
+        bits = (static_cast<uint64_t>(hi) << 32) | lo;
+    } else {
+        for (int dy = -rh; dy <= rh; ++dy) {
+            const float* row = c + dy * tw;
+            for (int dx = -rw; dx <= rw; ++dx) {
+                if (dx == 0 && dy == 0) continue;
+                bits = (bits << 1) | (row[dx] < center ? 1ull : 0ull);
+            }
         }
     }
     out[static_cast<size_t>(y) * w + x] = bits;
@@ -1761,8 +1788,11 @@ void census_pair(dco_ctx* ctx, const float* left, const float* right, int w, int
                  uint64_t* out_l, uint64_t* out_r) {
     const int rw = ww / 2, rh = wh / 2;
     const size_t smem = static_cast<size_t>(32 + 2 * rw) * (8 + 2 * rh) * sizeof(float);
-    k_census_tiled<<<dim3((w + 31) / 32, (h + 7) / 8, 2), dim3(32, 8), smem, ctx->stream>>>(left, right, w, h, rw,
-                                                                                           rh, out_l, out_r);
+    const dim3 grid((w + 31) / 32, (h + 7) / 8, 2);
+    if (rw == 4 && rh == 3)
+        k_census_tiled<4, 3><<<grid, dim3(32, 8), smem, ctx->stream>>>(left, right, w, h, rw, rh, out_l, out_r);
+    else
+        k_census_tiled<<<grid, dim3(32, 8), smem, ctx->stream>>>(left, right, w, h, rw, rh, out_l, out_r);
     launched(ctx, "k_census_tiled");
 }
 
