@@ -488,12 +488,17 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
     double o[2] = {0.0, 0.0};
-    for (int i = base + t; i < base + size; i += THREADS) {
-        int xx = i % w, y = i / w;
-        double xsi = __ldcg(a.xs + i);
-        o[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
-        o[1] += a.rhs[i] * xsi;
-    }
+    // the thread's elements in order, unrolled so their loads overlap
+    static_for<0, EPT>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        if (DCO_OK(k)) {
+            const int i = base + t + KO(k);
+            const int xx = i % w, y = i / w;
+            const double xsi = __ldcg(a.xs + i);
+            o[0] += xsi * apply_at(a.diag, a.ch, a.cv, a.xs, w, h, i, xx, y);
+            o[1] += a.rhs[i] * xsi;
+        }
+    });
     barrier_reduce<2>(o, bar, a.part, gen, sm, o);
     if (a.dbg && t == 0 && blockIdx.x == 0) {  // globaltimer: setup / teardown split (DCO_PCG_DEBUG)
         unsigned long long gt_;
