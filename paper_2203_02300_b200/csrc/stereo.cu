@@ -138,6 +138,40 @@ __global__ void k_cross_arms_raw(const float* __restrict__ img, int w, int h, in
     raw[3 * n + i] = static_cast<uint8_t>(grow_arm(img, w, h, x, y, 0, 1, l1, l2, tau1, tau2));
 }
 
+// The same arms with float compares: for a float diff and a double tau,
+// (double)diff >= tau  <=>  diff >= tf, tf the smallest float >= tau (host,
+// arm_threshold), so no conversion or FP64 compare per step; the loop splits
+// at l2 instead of selecting tau per step, and walks a pointer.
+__device__ __forceinline__ int grow_arm_f(const float* p, long long step, float center, int lim, int l2, float t1,
+                                          float t2) {
+    int l = 0;
+    const int n1 = min(lim, l2);
+    while (l < n1) {
+        p += step;
+        if (fabsf(*p - center) >= t1) return l;
+        ++l;
+    }
+    while (l < lim) {
+        p += step;
+        if (fabsf(*p - center) >= t2) return l;
+        ++l;
+    }
+    return l;
+}
+__global__ void k_cross_arms_f(const float* __restrict__ img, int w, int h, int l1, int l2, float t1, float t2,
+                               uint8_t* __restrict__ raw) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    if (x >= w || y >= h) return;
+    const size_t n = static_cast<size_t>(w) * h, i = static_cast<size_t>(y) * w + x;
+    const float* p = img + i;
+    const float c = *p;
+    raw[i] = static_cast<uint8_t>(grow_arm_f(p, -1, c, min(l1, x), l2, t1, t2));
+    raw[n + i] = static_cast<uint8_t>(grow_arm_f(p, 1, c, min(l1, w - 1 - x), l2, t1, t2));
+    raw[2 * n + i] = static_cast<uint8_t>(grow_arm_f(p, -static_cast<long long>(w), c, min(l1, y), l2, t1, t2));
+    raw[3 * n + i] = static_cast<uint8_t>(grow_arm_f(p, w, c, min(l1, h - 1 - y), l2, t1, t2));
+}
+
 // smooth_arm_channel, stereo.cpp:30-48: 3x3 clamped median (5th order
 // statistic), clamped back to the raw reach. blockIdx.z = channel.
 __global__ void k_arm_median(const uint8_t* __restrict__ raw, int w, int h, uint8_t* __restrict__ a0,
@@ -1766,10 +1800,23 @@ void build_cross_windows(dco_ctx* ctx, const float* img, int w, int h, const dco
     require(cfg->cross_arm_l1 <= 255, "build_cross_windows: cross_arm_l1 must fit the u8 arms");
     uint8_t* raw = static_cast<uint8_t*>(scratch(ctx, S_ARM_RAW, static_cast<size_t>(w) * h * 4));
     dim3 b(32, 8);
-    k_cross_arms_raw<<<grid2(w, h, b), b, 0, ctx->stream>>>(img, w, h, cfg->cross_arm_l1,
-                                                            cfg->cross_arm_l2, cfg->cross_color_tau,
-                                                            cfg->cross_color_tau2, raw);
-    launched(ctx, "k_cross_arms_raw");
+    if (!getenv("DCO_ARMS_F64")) {
+        // the smallest float >= tau: (double)diff >= tau <=> diff >= it
+        auto arm_threshold = [](double tau) {
+            float f = static_cast<float>(tau);
+            if (static_cast<double>(f) < tau) f = nextafterf(f, INFINITY);
+            return f;
+        };
+        k_cross_arms_f<<<grid2(w, h, b), b, 0, ctx->stream>>>(img, w, h, cfg->cross_arm_l1, cfg->cross_arm_l2,
+                                                              arm_threshold(cfg->cross_color_tau),
+                                                              arm_threshold(cfg->cross_color_tau2), raw);
+        launched(ctx, "k_cross_arms_f");
+    } else {
+        k_cross_arms_raw<<<grid2(w, h, b), b, 0, ctx->stream>>>(img, w, h, cfg->cross_arm_l1,
+                                                                cfg->cross_arm_l2, cfg->cross_color_tau,
+                                                                cfg->cross_color_tau2, raw);
+        launched(ctx, "k_cross_arms_raw");
+    }
     dim3 g = grid2(w, h, b);
     g.z = 4;
     k_arm_median<<<g, b, 0, ctx->stream>>>(raw, w, h, l, r, u, d);
