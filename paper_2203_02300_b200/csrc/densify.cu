@@ -40,16 +40,7 @@ __device__ __forceinline__ double fused_conf(const float* mf, int qw, int qh, in
     return isfinite(v) ? static_cast<double>(v) : 0.0;
 }
 
-// smoothness_weight, densify.cpp:26-35 (q is the right or lower neighbour).
-__device__ __forceinline__ double smooth_w(const uint8_t* e, const float* mf, int qw, int qh,
-                                           const float* mi, int w, int px, int py, int qx, int qy) {
-    size_t ip = static_cast<size_t>(py) * w + px, iq = static_cast<size_t>(qy) * w + qx;
-    int on = (e[ip] ? 1 : 0) + (e[iq] ? 1 : 0);
-    if (on == 1) return 0.0;
-    double sp = fused_conf(mf, qw, qh, px, py) * mi[ip];
-    double sq = fused_conf(mf, qw, qh, qx, qy) * mi[iq];
-    return dmax0(1.0 - dmin(sp, sq));
-}
+// smoothness_weight, densify.cpp:26-35: smooth_w_s in k_assemble.
 
 struct AsmArgs {
     int w, h, qw, qh;
@@ -70,11 +61,37 @@ struct AsmArgs {
 };
 
 // assemble_system per-pixel part, densify.cpp:70-114.
-__global__ void k_assemble(AsmArgs a) {
+// One 32x8 block per tile; s = fused_conf * m_i and the contour flag of the
+// tile and its one-pixel halo are computed once into shared memory, so each
+// of the four edge weights reads them there (smoothness_weight would compute
+// each endpoint's s twice per edge and every s four times per frame).
+__device__ __forceinline__ double smooth_w_s(uint8_t ep, uint8_t eq, double sp, double sq) {
+    if ((ep ? 1 : 0) + (eq ? 1 : 0) == 1) return 0.0;  // densify.cpp:26-35
+    return dmax0(1.0 - dmin(sp, sq));
+}
+__global__ void __launch_bounds__(256) k_assemble(AsmArgs a) {
+    __shared__ double s_s[10][34];
+    __shared__ uint8_t s_e[10][34];
+    const int w = a.w, h = a.h;
+    const int bx0 = blockIdx.x * blockDim.x - 1, by0 = blockIdx.y * blockDim.y - 1;
+    for (int k = threadIdx.y * blockDim.x + threadIdx.x; k < 10 * 34; k += blockDim.x * blockDim.y) {
+        const int ty = k / 34, tx = k - ty * 34;
+        const int gx = bx0 + tx, gy = by0 + ty;
+        double sv = 0.0;
+        uint8_t ev = 0;
+        if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
+            const size_t ip = static_cast<size_t>(gy) * w + gx;
+            ev = a.edges[ip];
+            sv = fused_conf(a.mf, a.qw, a.qh, gx, gy) * a.mi[ip];
+        }
+        s_s[ty][tx] = sv;
+        s_e[ty][tx] = ev;
+    }
+    __syncthreads();
     int x = blockIdx.x * blockDim.x + threadIdx.x;
     int y = blockIdx.y * blockDim.y + threadIdx.y;
-    if (x >= a.w || y >= a.h) return;
-    const int w = a.w, h = a.h;
+    if (x >= w || y >= h) return;
+    const int tx = threadIdx.x + 1, ty = threadIdx.y + 1;
     size_t i = static_cast<size_t>(y) * w + x;
     if (a.pre && a.pre_valid && *a.pre_valid == 0) a.pre = nullptr;
     const double two_ls = 2.0 * a.lambda_s;
@@ -96,15 +113,17 @@ __global__ void k_assemble(AsmArgs a) {
         rhs += a.lambda_s2 * dp;
         anch = 1;
     }
-    if (y > 0) diag += two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x, y - 1, x, y);
-    if (x > 0) diag += two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x - 1, y, x, y);
+    const uint8_t e0 = s_e[ty][tx];
+    const double s0 = s_s[ty][tx];
+    if (y > 0) diag += two_ls * smooth_w_s(s_e[ty - 1][tx], e0, s_s[ty - 1][tx], s0);
+    if (x > 0) diag += two_ls * smooth_w_s(s_e[ty][tx - 1], e0, s_s[ty][tx - 1], s0);
     double chv = 0.0, cvv = 0.0;
     if (x + 1 < w) {
-        chv = two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x, y, x + 1, y);
+        chv = two_ls * smooth_w_s(e0, s_e[ty][tx + 1], s0, s_s[ty][tx + 1]);
         diag += chv;
     }
     if (y + 1 < h) {
-        cvv = two_ls * smooth_w(a.edges, a.mf, a.qw, a.qh, a.mi, w, x, y, x, y + 1);
+        cvv = two_ls * smooth_w_s(e0, s_e[ty + 1][tx], s0, s_s[ty + 1][tx]);
         diag += cvv;
     }
     a.diag[i] = diag;
