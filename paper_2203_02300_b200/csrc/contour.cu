@@ -14,6 +14,8 @@
 //    holding a pixel with mag > t_high), so union-find connected components
 //    reproduce the reference's BFS exactly (contour.cpp:250-277).
 #include <math.h>
+#include <stdint.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "dco_libm.h"
@@ -295,10 +297,20 @@ __global__ void k_mag_norm(float* __restrict__ mag, size_t n, const unsigned* __
 
 // NMS (contour.cpp:205-236) + depth gate (:238-248); emits the hysteresis
 // classes: 0 none, 1 candidate (survives, mag >= t_low), 2 seed (mag > t_high).
+// The NMS sector of contour.cpp:217-232 depends on the float a = atan2f(gy,
+// gx) only through deg(a) = ((a < 0 ? a + pi : a) * 180) / pi in double,
+// which is monotone in a on each sign branch; the host finds, per branch, the
+// smallest float a whose deg reaches 22.5 / 67.5 / 112.5 / 157.5, so the
+// device compares a with those floats (no double math per pixel). Likewise
+// m >= t_low, m > t_high and conf < t_depth (float vs double) become float
+// compares against the nearest floats on the right side of the thresholds.
+struct NmsThresholds {
+    float pos[4], neg[4];   // sector boundaries for a >= 0 and a < 0
+    float low, high, depth;  // m >= low, m > high, conf < depth
+};
 __global__ void k_nms_gate(const float* __restrict__ gx, const float* __restrict__ gy,
                            const float* __restrict__ mag, int w, int h, const float* __restrict__ mf,
-                           int qw, int qh, double t_depth, double t_low, double t_high,
-                           uint8_t* __restrict__ cls) {
+                           int qw, int qh, const NmsThresholds th, uint8_t* __restrict__ cls) {
     int x = blockIdx.x * blockDim.x + threadIdx.x;
     int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= w || y >= h) return;
@@ -306,15 +318,20 @@ __global__ void k_nms_gate(const float* __restrict__ gx, const float* __restrict
     float m = mag[i];
     uint8_t c = 0;
     if (m > 0.0f) {
-        double angle = dco_atan2f(gy[i], gx[i]);
-        if (angle < 0) angle += kPi;
-        double deg = angle * 180.0 / kPi;
+        const float a = dco_atan2f(gy[i], gx[i]);
+        int sec;
+        if (isnan(a)) {
+            sec = 3;  // every deg comparison false: the reference's last branch
+        } else {
+            const float* t = a >= 0.0f ? th.pos : th.neg;
+            sec = a < t[0] ? 0 : a < t[1] ? 1 : a < t[2] ? 2 : a < t[3] ? 3 : 0;
+        }
         int ax, ay, bx, by;
-        if (deg < 22.5 || deg >= 157.5) {
+        if (sec == 0) {
             ax = x + 1; ay = y; bx = x - 1; by = y;
-        } else if (deg < 67.5) {
+        } else if (sec == 1) {
             ax = x + 1; ay = y + 1; bx = x - 1; by = y - 1;
-        } else if (deg < 112.5) {
+        } else if (sec == 2) {
             ax = x; ay = y + 1; bx = x; by = y - 1;
         } else {
             ax = x - 1; ay = y + 1; bx = x + 1; by = y - 1;
@@ -327,12 +344,85 @@ __global__ void k_nms_gate(const float* __restrict__ gx, const float* __restrict
         if (survives) {
             int mx = min(x / 2, qw - 1), my = min(y / 2, qh - 1);
             float conf = mf[static_cast<size_t>(my) * qw + mx];
-            if (!isfinite(conf) || conf < t_depth) survives = false;
+            if (!isfinite(conf) || conf < th.depth) survives = false;
         }
-        if (survives && m >= t_low) c = 1;
-        if (survives && m > t_high) c = 2;
+        if (survives && m >= th.low) c = 1;
+        if (survives && m > th.high) c = 2;
     }
     cls[i] = c;
+}
+
+// Every float a in [-4, 4] (and the NaNs): the sector from the thresholds
+// against the reference's double expression (tests/test_gpu_flow_contour.py).
+__global__ void k_nms_check(const NmsThresholds th, unsigned long long* bad) {
+    unsigned long long miss = 0;
+    for (unsigned long long u = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         u < (1ull << 32); u += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const float a = __uint_as_float(static_cast<unsigned>(u));
+        if (!(fabsf(a) <= 4.0f) && !isnan(a)) continue;
+        double angle = a;
+        if (angle < 0) angle += kPi;
+        const double deg = angle * 180.0 / kPi;
+        const int want = (deg < 22.5 || deg >= 157.5) ? 0 : deg < 67.5 ? 1 : deg < 112.5 ? 2 : 3;
+        int got;
+        if (isnan(a)) {
+            got = 3;
+        } else {
+            const float* t = a >= 0.0f ? th.pos : th.neg;
+            got = a < t[0] ? 0 : a < t[1] ? 1 : a < t[2] ? 2 : a < t[3] ? 3 : 0;
+        }
+        miss += got != want;
+    }
+    if (miss) atomicAdd(bad, miss);
+}
+
+// host: deg of contour.cpp:217-219 for the float atan2 value a
+double nms_deg(float a) {
+    double angle = a;
+    if (angle < 0) angle += kPi;
+    return angle * 180.0 / kPi;
+}
+int32_t float_key(float f) {  // order-preserving int of a non-NaN float
+    int32_t i;
+    memcpy(&i, &f, 4);
+    return i >= 0 ? i : static_cast<int32_t>(0x80000000u - static_cast<uint32_t>(i));
+}
+float key_float(int32_t k) {
+    int32_t i = k >= 0 ? k : static_cast<int32_t>(0x80000000u - static_cast<uint32_t>(k));
+    float f;
+    memcpy(&f, &i, 4);
+    return f;
+}
+// the smallest float a in [lo, hi] with nms_deg(a) >= b (hi's successor if none)
+float nms_bound(float lo, float hi, double b) {
+    int64_t l = float_key(lo), r = static_cast<int64_t>(float_key(hi)) + 1;  // answer in [l, r]
+    while (l < r) {
+        const int64_t mid = l + (r - l) / 2;
+        if (nms_deg(key_float(static_cast<int32_t>(mid))) >= b) r = mid; else l = mid + 1;
+    }
+    return key_float(static_cast<int32_t>(l));
+}
+float f_up(double t) {  // smallest float >= t
+    float f = static_cast<float>(t);
+    if (static_cast<double>(f) < t) f = nextafterf(f, INFINITY);
+    return f;
+}
+float f_down(double t) {  // largest float <= t
+    float f = static_cast<float>(t);
+    if (static_cast<double>(f) > t) f = nextafterf(f, -INFINITY);
+    return f;
+}
+NmsThresholds nms_thresholds(const dco_config* cfg) {
+    NmsThresholds th;
+    const double b[4] = {22.5, 67.5, 112.5, 157.5};
+    for (int k = 0; k < 4; ++k) {
+        th.pos[k] = nms_bound(0.0f, INFINITY, b[k]);
+        th.neg[k] = nms_bound(-INFINITY, -1.4e-45f, b[k]);
+    }
+    th.low = f_up(cfg->t_low);
+    th.high = f_down(cfg->t_high);
+    th.depth = f_up(cfg->t_depth);
+    return th;
 }
 
 // ------------------------------------------------------------- hysteresis --
@@ -491,8 +581,7 @@ void extract_depth_contours_prefiltered(dco_ctx* ctx, const float* blurred, int 
     launched(ctx, "k_sobel");
     k_mag_norm<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(mag, n, peak, m_i);
     launched(ctx, "k_mag_norm");
-    k_nms_gate<<<grid2(w, h, b), b, 0, ctx->stream>>>(gx, gy, mag, w, h, mf, qw, qh, cfg->t_depth,
-                                                      cfg->t_low, cfg->t_high, cls);
+    k_nms_gate<<<grid2(w, h, b), b, 0, ctx->stream>>>(gx, gy, mag, w, h, mf, qw, qh, nms_thresholds(cfg), cls);
     launched(ctx, "k_nms_gate");
     k_uf_init<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(cls, n, parent, seeded);
     launched(ctx, "k_uf_init");
@@ -549,6 +638,18 @@ int dco_extract_depth_contours(dco_ctx* ctx, const float* gray, int w, int h, co
         gaussian_blur(ctx, gray, w, h, cfg->gauss_sigma, blurred);
         extract_depth_contours_prefiltered(ctx, blurred, w, h, mf, qw, qh, cfg, edges, m_i);
     });
+}
+
+__attribute__((visibility("default"))) int dco_debug_nms_check(unsigned long long* mismatches) {
+    dco_config cfg;
+    dco_config_default(&cfg);
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, 8) != cudaSuccess) return DCO_CUDA;
+    cudaMemset(d, 0, 8);
+    dco_gpu::k_nms_check<<<1184, 256>>>(dco_gpu::nms_thresholds(&cfg), d);
+    const cudaError_t e = cudaMemcpy(mismatches, d, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? DCO_OK : DCO_CUDA;
 }
 
 }  // extern "C"

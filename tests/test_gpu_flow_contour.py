@@ -205,3 +205,21 @@ def test_flow_nonfinite_and_pinned(gpu, ref):
         u, v = ref.compute_flow(a, b, cfg)
         gu, gv = gpu.compute_flow(T(a), T(b), cfg)
         assert bits_equal(N(gu), u) and bits_equal(N(gv), v), (w, h)
+
+
+def test_nms_sector_thresholds_exhaustive(gpu):
+    """k_nms_gate classifies the gradient direction by comparing the float
+    atan2f value with per-branch float thresholds found on the host; for every
+    float in [-4, 4] and the NaNs, the sector equals the reference's double
+    expression (contour.cpp:217-232: (a < 0 ? a + pi : a) * 180 / pi against
+    22.5 / 67.5 / 112.5 / 157.5)."""
+    import ctypes
+
+    from paper_2203_02300_b200 import native
+
+    fn = native.load().dco_debug_nms_check
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    bad = ctypes.c_ulonglong(1)
+    assert fn(ctypes.byref(bad)) == 0
+    assert bad.value == 0
