@@ -31,8 +31,6 @@ __device__ __forceinline__ float clampf(float v, float lo, float hi) {
 // std::max(a, b) for floats: (a < b) ? b : a
 __device__ __forceinline__ float stdmaxf(float a, float b) { return (a < b) ? b : a; }
 
-__device__ __forceinline__ float qnan() { return __int_as_float(0x7fc00000); }
-
 // ------------------------------------------------------------ polar / amp --
 // flow_to_polar, contour.cpp:10-25.
 __global__ void k_polar(const float* __restrict__ u, const float* __restrict__ v, size_t n,
