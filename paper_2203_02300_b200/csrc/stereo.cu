@@ -1123,11 +1123,19 @@ __global__ void k_ref_vminmax(const float* __restrict__ cur, int w, int h, const
     const int y0 = y - U[i], y1 = y + D[i];
     int lo = 0x7fff, hi = -1;
     bool three = false;
-    for (int yy = y0; yy <= y1; ++yy) {
-        const uint2 v = mm[static_cast<size_t>(yy) * w + x];
-        lo = min(lo, static_cast<int>(v.x & 0xffffu));
-        hi = max(hi, static_cast<int>(static_cast<short>(v.x >> 16)));
-        three |= (v.y >> 16) != 0;
+    // kB rows' loads in flight at a time (min / max / or: any order)
+    constexpr int kB = 8;
+    for (int yb = y0; yb <= y1; yb += kB) {
+        uint2 v[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j)
+            v[j] = yb + j <= y1 ? mm[static_cast<size_t>(yb + j) * w + x] : make_uint2(0x7fffu | 0xffff0000u, 0u);
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            lo = min(lo, static_cast<int>(v[j].x & 0xffffu));
+            hi = max(hi, static_cast<int>(static_cast<short>(v[j].x >> 16)));
+            three |= (v[j].y >> 16) != 0;
+        }
     }
     if (lo == hi) {  // one bin in the region: it is the mode
         next[i] = static_cast<float>(lo);
