@@ -385,10 +385,18 @@ __global__ void k_region_size(const uint8_t* __restrict__ L, const uint8_t* __re
     int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= w || y >= h) return;
     size_t i = static_cast<size_t>(y) * w + x;
-    int s = 0;
-    for (int yy = y - U[i]; yy <= y + D[i]; ++yy) {
-        size_t j = static_cast<size_t>(yy) * w + x;
-        s += L[j] + R[j] + 1;
+    int s = 0;  // region_size (stereo.cpp:157-177): integer, any order
+    const int y1 = y + D[i];
+    constexpr int kB = 8;  // rows' loads in flight at a time
+    for (int yb = y - U[i]; yb <= y1; yb += kB) {
+        int v[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const size_t q = static_cast<size_t>(yb + j) * w + x;
+            v[j] = yb + j <= y1 ? L[q] + R[q] + 1 : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) s += v[j];
     }
     region[i] = s;
 }
@@ -535,10 +543,18 @@ __global__ void k_region_pack(const uint8_t* __restrict__ L, const uint8_t* __re
     int y = blockIdx.y * blockDim.y + threadIdx.y;
     if (x >= w || y >= h) return;
     size_t i = static_cast<size_t>(y) * w + x;
-    int s = 0;
-    for (int yy = y - U[i]; yy <= y + D[i]; ++yy) {
-        size_t j = static_cast<size_t>(yy) * w + x;
-        s += L[j] + R[j] + 1;
+    int s = 0;  // region_size (stereo.cpp:157-177): integer, any order
+    const int y1 = y + D[i];
+    constexpr int kB = 8;  // rows' loads in flight at a time
+    for (int yb = y - U[i]; yb <= y1; yb += kB) {
+        int v[kB];
+#pragma unroll
+        for (int j = 0; j < kB; ++j) {
+            const size_t q = static_cast<size_t>(yb + j) * w + x;
+            v[j] = yb + j <= y1 ? L[q] + R[q] + 1 : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kB; ++j) s += v[j];
     }
     hinfo[i] = L[i] | (static_cast<uint32_t>(R[i]) << 8);
     vinfo[i] = U[i] | (static_cast<uint32_t>(D[i]) << 8) | (static_cast<uint32_t>(s) << 16);
