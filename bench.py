@@ -49,7 +49,7 @@ CONFIG = {
     "width": W, "height": H, "disparities": D,
     "frames": "synthetic stereo video (paper_2203_02300_b200.synth), independent streams, d_pre chain active",
     "virtual_layer": "cube mesh (0.3 m) rendered per frame under a per-frame pose",
-    "l2": "GPU arm: flushed (160 MiB memset, L2 is 126 MB) before every frame, inside the timed region",
+    "l2": "GPU arm: flushed (160 MiB written, L2 is 126 MB) before every frame, inside the timed region",
     "parallelism": "frames shard as independent streams: 8 per GPU x N GPUs (GPU arm), one per host core "
                    "(reference arm); no data-path collective",
 }
@@ -369,13 +369,15 @@ def run_ours(args, world, rank, local):
             st = dco.Stream(W, H, cfg, ctx=dco.new_context(tstreams[s]))
             st.set_mesh(mesh_v, mesh_t, mesh_c)
             streams.append(st)
-    flush = [torch.empty(160 << 20, dtype=torch.uint8, device="cuda") for _ in range(S)]  # > the 126 MB L2
+    # > the 126 MB L2; written as int32 words (fill_ on a 4-byte view runs at ~6.6 TB/s, zero_ on
+    # bytes at ~3.7: the same 160 MiB written, half the time)
+    flush = [torch.empty(40 << 20, dtype=torch.int32, device="cuda") for _ in range(S)]
     pos = [0] * S
 
     def push(s, want=False):
         with torch.cuda.stream(tstreams[s]):
             streams[s].set_next_pose(frame_pose(pos[s]))
-            flush[s].zero_()  # L2 flush before every frame, inside the timed region
+            flush[s].fill_(pos[s])  # L2 flush before every frame, inside the timed region
             r = streams[s].push_gray8(dev_l[s][pos[s] % nframes], dev_r[s][pos[s] % nframes], want_result=want)
         pos[s] += 1
         return r
