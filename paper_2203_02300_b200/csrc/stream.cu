@@ -29,7 +29,7 @@ void transform_mesh(dco_ctx* ctx, const float* verts, int nv, const double* pose
 void render_virtual(dco_ctx* ctx, const float* verts, const int* tris, const float* colors, int nt, double focal_px,
                     double cx, double cy, int w, int h, float* rgb, float* depth);
 // slice-major stereo core of the frame loop (stereo_slices.cu)
-bool stereo_slices_supported(int max_arm);
+bool stereo_slices_supported(int max_arm, int qh);
 void cost_volume_slices(dco_ctx* ctx, const float* left, const float* right, int w, int h, const uint8_t* l,
                         const uint8_t* r, const uint8_t* u, const uint8_t* d, const dco_config* cfg, int max_arm,
                         float* cost, int* rect);
@@ -309,7 +309,7 @@ void stereo_chain(dco_stream* s, const float* lq, const float* rq, float* out) {
     const size_t nq = static_cast<size_t>(qw) * qh;
     uint8_t *L = s->arms, *R = L + nq, *U = R + nq, *D = U + nq;
     build_cross_windows(ctx, lq, qw, qh, cfg, L, R, U, D);
-    if (stereo_slices_supported(cfg->cross_arm_l1)) {
+    if (stereo_slices_supported(cfg->cross_arm_l1, s->qh)) {
         int* rect = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, 2 * static_cast<size_t>(s->nd) * sizeof(int)));
         cost_volume_slices(ctx, lq, rq, qw, qh, L, R, U, D, cfg, cfg->cross_arm_l1, s->cost, rect);
         aggregate_slices(ctx, s->cost, qw, qh, s->nd, L, R, U, D, cfg->cross_arm_l1, rect, s->agg);
@@ -339,7 +339,7 @@ void run_frame(dco_stream* s, dco_frame_result* res) {
     // --- stereo on the middle pair (pipeline.cpp:184-195)
     build_cross_windows(ctx, s->left_q[mid], qw, qh, cfg, L, R, U, D);
     s->mark(DCO_SPAN_CROSS + 1);
-    if (stereo_slices_supported(cfg->cross_arm_l1)) {
+    if (stereo_slices_supported(cfg->cross_arm_l1, s->qh)) {
         // slice-major cost volume + exact fixed-point aggregation (stereo_slices.cu)
         int* rect = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, 2 * static_cast<size_t>(s->nd) * sizeof(int)));
         cost_volume_slices(ctx, s->left_q[mid], s->right_q[mid], qw, qh, L, R, U, D, cfg, cfg->cross_arm_l1, s->cost,
@@ -755,7 +755,7 @@ int dco_stream_views(const dco_stream* s, dco_frame_views* v) {
     v->flow_future_v = s->flow + 3 * nq;
     v->cost_volume = s->cost;
     v->aggregated = s->agg;
-    v->volume_layout = stereo_slices_supported(s->cfg.cross_arm_l1) ? 1 : 0;
+    v->volume_layout = stereo_slices_supported(s->cfg.cross_arm_l1, s->qh) ? 1 : 0;
     v->num_disparities = s->nd;
     return DCO_OK;
 }
@@ -833,7 +833,7 @@ int dco_stereo_sparse_depth(dco_ctx* ctx, const float* left_q, const float* righ
         float* d1 = d0 + nq;
         uint8_t *L = arms, *R = arms + nq, *U = arms + 2 * nq, *D = arms + 3 * nq;
         build_cross_windows(ctx, left_q, w, h, cfg, L, R, U, D);
-        if (stereo_slices_supported(cfg->cross_arm_l1)) {
+        if (stereo_slices_supported(cfg->cross_arm_l1, h)) {
             int* rect = static_cast<int*>(scratch(ctx, S_FLAG_SLICE, 2 * static_cast<size_t>(nd) * sizeof(int)));
             cost_volume_slices(ctx, left_q, right_q, w, h, L, R, U, D, cfg, cfg->cross_arm_l1, cost, rect);
             aggregate_slices(ctx, cost, w, h, nd, L, R, U, D, cfg->cross_arm_l1, rect, agg);
