@@ -728,16 +728,28 @@ long long* g_pcg_dbg = nullptr;
 constexpr int kDbgLen = 1280 + 64 * 1024 * 3 + 1024;  // + per-block globaltimer stamps, per-block SM ids
 
 // "k_pcg_tmem<7>"-style instance names with stable storage (dco_last_solver)
-const char* instance_name(const char* base, int ept) {
+const char* instance_name(const char* base, int ept, int threads = 0) {
     static std::mutex mu;
     static std::set<std::string> names;
     std::lock_guard<std::mutex> lock(mu);
-    return names.insert(std::string(base) + "<" + std::to_string(ept) + ">").first->c_str();
+    std::string s = std::string(base) + "<" + std::to_string(ept);
+    if (threads) s += ", " + std::to_string(threads);
+    return names.insert(s + ">").first->c_str();
 }
 
 typedef void (*OnchipKernel)(CGArgs, int, GridBar*);
 constexpr int kOnchipThreadsUsed = 1024;
 constexpr int kOnchipSmemMax = 222 * 1024;  // + 2.6 KB static reduction scratch <= 227 KB
+// k_pcg_tmem<E, 640>: 20 warps (5 per TMEM lane quarter, 96 columns each), 96 registers
+constexpr int kTmem640 = 640;
+OnchipKernel tmem640_for(int ept) {
+    switch (ept) {
+        case 9: return k_pcg_tmem<9, kTmem640>;
+        case 10: return k_pcg_tmem<10, kTmem640>;
+        case 11: return k_pcg_tmem<11, kTmem640>;  // EPT 12: a chunk > 7040, more shared memory than a CTA has
+        default: return nullptr;
+    }
+}
 OnchipKernel tmem_for(int ept) {
     switch (ept) {
         case 1: return k_pcg_tmem<1>;
@@ -931,6 +943,19 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     // the registers + shared-memory variant
     const bool no_tmem = getenv("DCO_PCG_NO_TMEM") != nullptr;
     OnchipKernel kern = no_tmem ? onchip_for(threads, ept) : tmem_for(ept);
+    // systems whose 1024-thread chunk needs 6 or more slots run k_pcg_tmem<E, 640>
+    // (20 warps, 96 registers, 96 TMEM columns per warp): 0.708 against 0.762 ms
+    // at config B (EPT 10 against 7; 896 / 768 / 512 / 384 threads: 0.738 / 0.750
+    // / 0.730 / 0.800). DCO_PCG_1024=1 keeps 1024 threads.
+    int tthreads = threads, tept = ept;
+    if (!no_tmem && ept >= 6 && !getenv("DCO_PCG_1024")) {
+        const int e640 = (chunk + kTmem640 - 1) / kTmem640;
+        if (OnchipKernel k640 = tmem640_for(e640)) {
+            kern = k640;
+            tthreads = kTmem640;
+            tept = e640;
+        }
+    }
     // DCO_PCG_FORCE_BIG=1 / DCO_PCG_FORCE_STREAM=1 (tests): the large-frame /
     // any-size kernel even when the state fits on chip
     const bool force_stream = getenv("DCO_PCG_FORCE_STREAM") != nullptr;
@@ -962,10 +987,11 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
         cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
         void* params[] = {&a, &chunk_arg, &bar};
-        launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(threads),
+        launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(tthreads),
                                       params, smem);
         launched(ctx, no_tmem ? "k_pcg_onchip" : "k_pcg_tmem");
-        ctx->last_solver = instance_name(no_tmem ? "k_pcg_onchip" : "k_pcg_tmem", ept);
+        ctx->last_solver = tthreads == kTmem640 ? instance_name("k_pcg_tmem", tept, kTmem640)
+                                                : instance_name(no_tmem ? "k_pcg_onchip" : "k_pcg_tmem", ept);
         return;
     }
     // larger frames: p on chip, q/rs in TMEM, r in registers, the rest L2-resident

@@ -83,10 +83,13 @@ __device__ __forceinline__ void d2u(double d, uint32_t& lo, uint32_t& hi) {
     hi = static_cast<uint32_t>(__double2hiint(d));
 }
 
-template <int EPT>
-__global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridBar* bar) {
-    constexpr int THREADS = 1024;
-    static_assert(EPT >= 1 && EPT <= 8, "8 warps per TMEM lane quarter x 8*EPT columns <= 512");
+// THREADS = 896 (28 warps, 7 per lane quarter, 72 TMEM columns each): up to 72
+// registers per thread and room in TMEM for the x of every slot up to EPT 7.
+template <int EPT, int THREADS = 1024>
+__global__ void __launch_bounds__(THREADS, 1) k_pcg_tmem(CGArgs a, int chunk, GridBar* bar) {
+    constexpr int CPW = THREADS == 1024 ? 64 : ((512 / (THREADS / 128)) & ~7);  // TMEM columns per warp
+    static_assert(THREADS % 128 == 0 && THREADS <= 1024, "whole lane quarters");
+    static_assert(EPT >= 1 && 8 * EPT <= CPW, "8*EPT TMEM columns per warp");
     extern __shared__ double sx[];  // p [w + chunk + w], coup_h, coup_v, prec [chunk] each
     __shared__ double sm[32 * 16];
     __shared__ double s_w1[32 * 4];  // per-warp P1 sums
@@ -151,10 +154,12 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tm = tm_lane_col(s_tmem, warp);  // this warp's column 0, lane base
+    // this warp's column 0, lane base: quarter warp % 4, column range (warp / 4) * CPW
+    const uint32_t tm = s_tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                        static_cast<uint32_t>((warp >> 2) * CPW);
     // x of the first XT slots lives in the spare columns 8*EPT.. (2 per slot),
     // the rest in registers
-    constexpr int XT = (64 - 8 * EPT) / 2 < EPT ? (64 - 8 * EPT) / 2 : EPT;
+    constexpr int XT = (CPW - 8 * EPT) / 2 < EPT ? (CPW - 8 * EPT) / 2 : EPT;
     const uint32_t tmx = tm + 8 * EPT;
     if (a.dbg && t == 0 && blockIdx.x == 0) {  // globaltimer: setup / teardown split (DCO_PCG_DEBUG)
         unsigned long long gt_;
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(1024, 1) k_pcg_tmem(CGArgs a, int chunk, GridB
             // halo rows [-w, 0) and [size, size + w): p_iter of the neighbours,
             // recomputed with the owner's FMA sequence
             {
-                constexpr int kHalo = 3;
+                constexpr int kHalo = THREADS <= 640 ? 4 : 3;  // 2w <= kHalo * THREADS at w = 1280
                 double h0[kHalo], h1[kHalo], h2[kHalo], h3[kHalo];
 #pragma unroll
                 for (int u = 0; u < kHalo; ++u) {

@@ -6,15 +6,16 @@ these pin the instances the bench and the large configs actually dispatch:
 * config B (1280x720, D=128): whole composited frames through dco_stream
   against the reference's run_pipeline body (pipeline.cpp:183-258), the first
   composited frame (no d_pre) and a steady one (d_pre chain). The solve is
-  k_pcg_tmem<7>, whose x slots 4..6 live in registers (pcg_tmem.cuh XT=4).
+  k_pcg_tmem<10, 640> (640 threads; x slots 8..9 in registers).
 * config A (640x480, D=64): the same, k_pcg_tmem<3>.
 * config C (1920x1080, D=192): the stream's own assembled system solved by
   k_pcg_big<19> against the reference's solve_dense_depth
   (densify.cpp:141-222) on the same inputs.
 * config D (3840x2160, D=256): the same for k_pcg_stream<512,2>, steady
   frame (d_pre from the stream's previous frame).
-* every k_pcg_tmem slot count (EPT 2..7; 1 is the small-system tests') against the oracle on one system,
-  reached with DCO_PCG_BLOCKS (fewer, fuller blocks).
+* every k_pcg_tmem slot count (EPT 2..7 at 1024 threads, 9..11 at 640; 1 is
+  the small-system tests') against the oracle on one system, reached with
+  DCO_PCG_BLOCKS (fewer, fuller blocks).
 
 Bars: sparse, edges, m_fuse, m_i, flow, composite outside the
 solver tolerance band: bit-exact; dense max-abs <= 1e-5 m, RMS <= 1e-6 m;
@@ -103,7 +104,7 @@ def _stream_vs_reference(gpu, ref, W, H, D, solver, frames=4, seed=61):
 
 def test_config_b_stream_frames_vs_reference(gpu, ref):
     """1280x720 D=128 (the bench's frame): first + steady composited frame."""
-    rep = _stream_vs_reference(gpu, ref, 1280, 720, 128, "k_pcg_tmem<7>")
+    rep = _stream_vs_reference(gpu, ref, 1280, 720, 128, "k_pcg_tmem<10, 640>")
     assert len(rep) == 2
     assert rep[0][1] > rep[1][1]  # the first frame has no d_pre: many more iterations
 
@@ -172,14 +173,29 @@ def _ceil(a, b):
 
 @pytest.mark.parametrize("ept", [2, 3, 4, 5, 6, 7])
 def test_every_tmem_slot_count_vs_reference(gpu, ref, ept, monkeypatch):
-    """k_pcg_tmem<EPT> for every reachable EPT on one real 640x360 system: the
-    largest grid whose chunk gives each of 1024 threads EPT slots, so the
-    register x slots (EPT 7, x slots 4..6) run at a size the oracle solves in
-    a second. (EPT 8 needs a chunk > 7168 unknowns, 229 KB of shared memory:
-    never dispatched.)"""
+    monkeypatch.setenv("DCO_PCG_1024", "1")  # the 1024-thread instances (EPT 6, 7 default to 640 threads)
+    _tmem_slot_case(gpu, ref, ept, 1024, "k_pcg_tmem<%d>" % ept, monkeypatch)
+
+
+@pytest.mark.parametrize("ept", [9, 10, 11])
+def test_every_tmem640_slot_count_vs_reference(gpu, ref, ept, monkeypatch):
+    """k_pcg_tmem<EPT, 640> (20 warps; XT = (96 - 8 EPT) / 2 x slots in TMEM,
+    the rest in registers) on the same 640x360 system, reached with
+    DCO_PCG_BLOCKS. (EPT 12 needs a chunk > 7040 unknowns: more shared memory
+    than a CTA has, never dispatched.)"""
+    _tmem_slot_case(gpu, ref, ept, 640, "k_pcg_tmem<%d, 640>" % ept, monkeypatch)
+
+
+def _tmem_slot_case(gpu, ref, ept, threads, name, monkeypatch):
+    """k_pcg_tmem<EPT(, threads)> on one real 640x360 system: the largest grid
+    whose chunk gives each thread EPT slots (and, for 640 threads, needs 6 or
+    more at 1024, where the dispatch takes 640), so the register x slots run at
+    a size the oracle solves in a second. (EPT 8 at 1024 threads needs a chunk
+    > 7168 unknowns, 229 KB of shared memory: never dispatched.)"""
     W, H = 640, 360
     n = W * H
-    blocks = max(b for b in range(1, 149) if _ceil(_ceil(n, b), 1024) == ept)
+    blocks = max(b for b in range(1, 149) if _ceil(_ceil(n, b), threads) == ept and
+                 (threads == 1024 or _ceil(_ceil(n, b), 1024) >= 6))
     assert _ceil(n, blocks) * 32 + 16 * W <= 222 * 1024
     cfg, o, pre, _, _ = _stream_system(gpu, W, H, 64, 4, seed=7)
     host = {k: N(v) for k, v in o.items()}
@@ -188,6 +204,6 @@ def test_every_tmem_slot_count_vs_reference(gpu, ref, ept, monkeypatch):
     monkeypatch.setenv("DCO_PCG_BLOCKS", str(blocks))
     sys = gpu.assemble_system(o["sparse"], o["edges"], o["m_fuse"], o["m_i"], pre, cfg)
     got, gst = gpu.solve_dense_depth(sys, cfg)
-    assert gpu.last_solver() == "k_pcg_tmem<%d>" % ept
+    assert gpu.last_solver() == name
     _dense_ok(N(got), want)
     assert abs(gst.iterations - st["iterations"]) <= 2
