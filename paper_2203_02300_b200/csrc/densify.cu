@@ -777,6 +777,20 @@ BigKernel share_for(int ept) {
         default: return nullptr;
     }
 }
+BigKernel big1024_for(int ept) {
+    switch (ept) {
+        case 8: return k_pcg_big<8, 1024, 64, false>;
+        case 9: return k_pcg_big<9, 1024, 64, false>;
+        case 10: return k_pcg_big<10, 1024, 64, false>;
+        case 11: return k_pcg_big<11, 1024, 64, false>;
+        case 12: return k_pcg_big<12, 1024, 64, false>;
+        case 13: return k_pcg_big<13, 1024, 64, false>;
+        case 14: return k_pcg_big<14, 1024, 64, false>;
+        case 15: return k_pcg_big<15, 1024, 64, false>;
+        case 16: return k_pcg_big<16, 1024, 64, false>;
+        default: return nullptr;
+    }
+}
 BigKernel big_for(int ept) {
     switch (ept) {
         case 9: return k_pcg_big<9, kBigThreads, kBigCols, false>;
@@ -998,19 +1012,28 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     {
         const int ept_b = (chunk + kBigThreads - 1) / kBigThreads;
         const size_t smem_b = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
-        BigKernel bk = big_for(ept_b < 9 ? 9 : ept_b);
+        // 1024 threads (EPT <= 16, 64 TMEM columns per warp) where the chunk
+        // fits, else 768 (EPT <= 21): at 1920x1080 3.31 against 3.79 ms
+        // (896 threads: 3.46, 640: 4.23). DCO_PCG_BIG768=1 keeps 768.
+        const int ept_k = std::max(8, (chunk + 1023) / 1024);
+        BigKernel bk = getenv("DCO_PCG_BIG768") ? nullptr : big1024_for(ept_k);
+        int bthreads = 1024, e = ept_k;
+        if (!bk) {
+            e = ept_b < 9 ? 9 : ept_b;
+            bk = big_for(e);
+            bthreads = kBigThreads;
+        }
         if (bk && !force_stream && smem_b <= kOnchipSmemMax && sms <= 1024 && !getenv("DCO_PCG_NO_BIG")) {
-            const int e = ept_b < 9 ? 9 : ept_b;
             smem_attr(ctx, bk, static_cast<int>(smem_b));
             int chunk_arg = chunk;
             GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
             cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
             double* hb = static_cast<double*>(scratch(ctx, S_TMP1, 7 * n * sizeof(double)));
             void* params[] = {&a, &chunk_arg, &bar, &hb};
-            launch_cooperative_serialized(ctx, reinterpret_cast<void*>(bk), dim3(sms), dim3(kBigThreads), params,
+            launch_cooperative_serialized(ctx, reinterpret_cast<void*>(bk), dim3(sms), dim3(bthreads), params,
                                           smem_b);
             launched(ctx, "k_pcg_big");
-            ctx->last_solver = instance_name("k_pcg_big", e);
+            ctx->last_solver = bthreads == 1024 ? instance_name("k_pcg_big", e, 1024) : instance_name("k_pcg_big", e);
             return;
         }
     }

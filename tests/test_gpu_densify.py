@@ -71,19 +71,20 @@ def _solve_both(gpu, ref, sparse, edges, m_fuse, m_i, pre, cfg):
     return N(got), gst, want, st
 
 
-VARIANT_ENV = {"tmem": None, "onchip": "DCO_PCG_NO_TMEM", "big": "DCO_PCG_FORCE_BIG", "share": "DCO_PCG_SHARE",
-               "stream": "DCO_PCG_FORCE_STREAM"}
+VARIANT_ENV = {"tmem": None, "onchip": "DCO_PCG_NO_TMEM", "big": "DCO_PCG_FORCE_BIG",
+               "big768": "DCO_PCG_FORCE_BIG,DCO_PCG_BIG768", "share": "DCO_PCG_SHARE", "stream": "DCO_PCG_FORCE_STREAM"}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANT_ENV))
 @pytest.mark.parametrize("seed,with_pre", [(5150, False), (5151, True), (77, False)])
 def test_solve_small_within_tolerance(gpu, ref, seed, with_pre, variant, monkeypatch):
     """Every solver variant: tmem (default), onchip (registers + shared memory,
-    DCO_PCG_NO_TMEM), big (x/xs/coefficients in L2, forced on a small system),
+    DCO_PCG_NO_TMEM), big (x/xs/coefficients in L2, forced on a small system;
+    1024 threads, and big768 the 768-thread instances),
     share (the co-residency kernel) and stream (every vector in global memory,
     the any-size path)."""
-    if VARIANT_ENV[variant]:
-        monkeypatch.setenv(VARIANT_ENV[variant], "1")
+    for env in filter(None, (VARIANT_ENV[variant] or "").split(",")):
+        monkeypatch.setenv(env, "1")
     cfg = Config(solver_tol=1e-12, solver_max_iter=3000)
     got, gst, want, st = _solve_both(gpu, ref, *random_inputs(16, 16, seed, with_pre), cfg)
     d = np.abs(got.astype(np.float64) - want)
@@ -96,8 +97,8 @@ def test_solve_small_within_tolerance(gpu, ref, seed, with_pre, variant, monkeyp
 def test_solve_scene_within_tolerance(gpu, ref, variant, monkeypatch):
     """A real frame's system (640x360 full res) with and without d_pre, on each
     solver variant."""
-    if VARIANT_ENV[variant]:
-        monkeypatch.setenv(VARIANT_ENV[variant], "1")
+    for env in filter(None, (VARIANT_ENV[variant] or "").split(",")):
+        monkeypatch.setenv(env, "1")
     cfg = Config(d_max=63)
     fs = [scene(ref, 640, 360, index=i, seed=61) for i in range(4)]
     q = [ref.downsample_half(f["left"]) for f in fs]

@@ -9,7 +9,7 @@ these pin the instances the bench and the large configs actually dispatch:
   k_pcg_tmem<10, 640> (640 threads; x slots 8..9 in registers).
 * config A (640x480, D=64): the same, k_pcg_tmem<3>.
 * config C (1920x1080, D=192): the stream's own assembled system solved by
-  k_pcg_big<19> against the reference's solve_dense_depth
+  k_pcg_big<14, 1024> against the reference's solve_dense_depth
   (densify.cpp:141-222) on the same inputs.
 * config D (3840x2160, D=256): the same for k_pcg_stream<512,2>, steady
   frame (d_pre from the stream's previous frame).
@@ -143,7 +143,7 @@ def _stream_system(gpu, W, H, D, frames, seed=61):
 
 
 @pytest.mark.parametrize("W,H,D,frames,solver", [
-    (1920, 1080, 192, 4, "k_pcg_big<19>"),
+    (1920, 1080, 192, 4, "k_pcg_big<14, 1024>"),
     (3840, 2160, 256, 4, "k_pcg_stream<512,2>"),
 ])
 def test_large_frame_solve_vs_reference(gpu, ref, W, H, D, frames, solver):
