@@ -750,6 +750,19 @@ OnchipKernel tmem640_for(int ept) {
         default: return nullptr;
     }
 }
+// k_pcg_tmem<E, 512>: 16 warps (4 per TMEM lane quarter, 128 columns each), 128 registers
+constexpr int kTmem512 = 512;
+OnchipKernel tmem512_for(int ept) {
+    switch (ept) {
+        case 5: return k_pcg_tmem<5, kTmem512>;
+        case 6: return k_pcg_tmem<6, kTmem512>;
+        case 7: return k_pcg_tmem<7, kTmem512>;
+        case 8: return k_pcg_tmem<8, kTmem512>;
+        case 9: return k_pcg_tmem<9, kTmem512>;
+        case 10: return k_pcg_tmem<10, kTmem512>;
+        default: return nullptr;
+    }
+}
 OnchipKernel tmem_for(int ept) {
     switch (ept) {
         case 1: return k_pcg_tmem<1>;
@@ -969,6 +982,15 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
             tthreads = kTmem640;
             tept = e640;
         }
+    } else if (!no_tmem && ept >= 3 && !getenv("DCO_PCG_1024")) {
+        // 3..5 slots at 1024 threads (config A: 0.470 ms at 512 threads against
+        // 0.539 at 1024; 768 / 640 / 384: 0.487 / 0.484 / 0.474)
+        const int e512 = (chunk + kTmem512 - 1) / kTmem512;
+        if (OnchipKernel k512 = tmem512_for(e512)) {
+            kern = k512;
+            tthreads = kTmem512;
+            tept = e512;
+        }
     }
     // DCO_PCG_FORCE_BIG=1 / DCO_PCG_FORCE_STREAM=1 (tests): the large-frame /
     // any-size kernel even when the state fits on chip
@@ -1004,8 +1026,8 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(tthreads),
                                       params, smem);
         launched(ctx, no_tmem ? "k_pcg_onchip" : "k_pcg_tmem");
-        ctx->last_solver = tthreads == kTmem640 ? instance_name("k_pcg_tmem", tept, kTmem640)
-                                                : instance_name(no_tmem ? "k_pcg_onchip" : "k_pcg_tmem", ept);
+        ctx->last_solver = tthreads != threads ? instance_name("k_pcg_tmem", tept, tthreads)
+                                               : instance_name(no_tmem ? "k_pcg_onchip" : "k_pcg_tmem", ept);
         return;
     }
     // larger frames: p on chip, q/rs in TMEM, r in registers, the rest L2-resident

@@ -7,7 +7,7 @@ these pin the instances the bench and the large configs actually dispatch:
   against the reference's run_pipeline body (pipeline.cpp:183-258), the first
   composited frame (no d_pre) and a steady one (d_pre chain). The solve is
   k_pcg_tmem<10, 640> (640 threads; x slots 8..9 in registers).
-* config A (640x480, D=64): the same, k_pcg_tmem<3>.
+* config A (640x480, D=64): the same, k_pcg_tmem<5, 512>.
 * config C (1920x1080, D=192): the stream's own assembled system solved by
   k_pcg_big<14, 1024> against the reference's solve_dense_depth
   (densify.cpp:141-222) on the same inputs.
@@ -111,7 +111,7 @@ def test_config_b_stream_frames_vs_reference(gpu, ref):
 
 def test_config_a_stream_frames_vs_reference(gpu, ref):
     """640x480 D=64 (BASELINE config A, the reference's CPU-runnable case)."""
-    rep = _stream_vs_reference(gpu, ref, 640, 480, 64, "k_pcg_tmem<3>")
+    rep = _stream_vs_reference(gpu, ref, 640, 480, 64, "k_pcg_tmem<5, 512>")
     assert len(rep) == 2
 
 
@@ -186,6 +186,14 @@ def test_every_tmem640_slot_count_vs_reference(gpu, ref, ept, monkeypatch):
     _tmem_slot_case(gpu, ref, ept, 640, "k_pcg_tmem<%d, 640>" % ept, monkeypatch)
 
 
+@pytest.mark.parametrize("ept", [5, 6, 7, 8, 9, 10])
+def test_every_tmem512_slot_count_vs_reference(gpu, ref, ept, monkeypatch):
+    """k_pcg_tmem<EPT, 512> (16 warps, 128 TMEM columns per warp), dispatched
+    for systems needing 3..5 slots at 1024 threads (config A), reached with
+    DCO_PCG_BLOCKS."""
+    _tmem_slot_case(gpu, ref, ept, 512, "k_pcg_tmem<%d, 512>" % ept, monkeypatch)
+
+
 def _tmem_slot_case(gpu, ref, ept, threads, name, monkeypatch):
     """k_pcg_tmem<EPT(, threads)> on one real 640x360 system: the largest grid
     whose chunk gives each thread EPT slots (and, for 640 threads, needs 6 or
@@ -194,8 +202,9 @@ def _tmem_slot_case(gpu, ref, ept, threads, name, monkeypatch):
     > 7168 unknowns, 229 KB of shared memory: never dispatched.)"""
     W, H = 640, 360
     n = W * H
+    k1024 = {1024: range(1, 9), 640: range(6, 9), 512: range(3, 6)}[threads]  # the dispatch's tiers
     blocks = max(b for b in range(1, 149) if _ceil(_ceil(n, b), threads) == ept and
-                 (threads == 1024 or _ceil(_ceil(n, b), 1024) >= 6))
+                 _ceil(_ceil(n, b), 1024) in k1024)
     assert _ceil(n, blocks) * 32 + 16 * W <= 222 * 1024
     cfg, o, pre, _, _ = _stream_system(gpu, W, H, 64, 4, seed=7)
     host = {k: N(v) for k, v in o.items()}
