@@ -121,7 +121,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_tmem(CGArgs a, int chunk, Gr
     unsigned gen = 0;
     double r[EPT], x[EPT];
     unsigned pub = 0;  // bit k: slot k lies in a row other blocks read as halo
+    // The host picks EPT = ceil(chunk / THREADS) with chunk = ceil(n / nb), so
+    // (EPT - 1) * THREADS <= chunk - 1 <= qn <= size: slots 0 .. EPT-2 are
+    // occupied in every thread of every block (DCO_FULL: only the last slot is
+    // tested). A launch breaking this is a host bug.
+    if (qn < (EPT - 1) * THREADS) __trap();
 #define DCO_OK(k) ((k) < nv)
+#define DCO_FULL(k) ((k) < EPT - 1 || (k) < nv)
 #define KO(k) ((k) * THREADS)
 
     if (a.dbg && t == 0 && blockIdx.x == 0) {  // kernel entry (DCO_PCG_DEBUG)
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_tmem(CGArgs a, int chunk, Gr
                 const double rsi = u2d(cur4[0], cur4[1]);
                 const double dg = u2d(cur4[2], cur4[3]);
                 double acc = 0.0;
-                if (DCO_OK(k)) {
+                if (DCO_FULL(k)) {
                     const int o = KO(k);
                     const int l = t + o;
                     const double pk = lds<8 * KO(k)>(aP);
@@ -518,6 +524,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_tmem(CGArgs a, int chunk, Gr
     }
 #undef STAMP
 #undef DCO_OK
+#undef DCO_FULL
 #undef KO
 }
 
