@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_tmem(CGArgs a, int chunk, Gr
                 double xsi = u2d(c4[2], c4[3]);
                 double rsi = u2d(c2[0], c2[1]);
                 double xk = k < XT ? u2d(cx[0], cx[1]) : x[k];
-                if (DCO_OK(k)) {
+                if (DCO_FULL(k)) {
                     const int o = KO(k);
                     double pk = lds<8 * KO(k)>(aP);
                     double ri = r[k];

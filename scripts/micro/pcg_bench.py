@@ -10,8 +10,9 @@ from paper_2203_02300_b200 import dco  # noqa: E402
 from paper_2203_02300_b200.config import Config  # noqa: E402
 from paper_2203_02300_b200.synth import StereoVideo  # noqa: E402
 
-W, H = 1280, 720
-cfg = Config(d_max=127)
+# usage: pcg_bench.py [W H D_MAX]  (default 1280 720 127)
+W, H, DMAX = (int(v) for v in sys.argv[1:4]) if len(sys.argv) >= 4 else (1280, 720, 127)
+cfg = Config(d_max=DMAX)
 vid = StereoVideo(W, H)
 s = dco.Stream(W, H, cfg)
 for i in range(4):
@@ -37,4 +38,9 @@ for cap in (0, 1, 10, 40, 80):
     torch.cuda.synchronize()
     print("cap %3d iters %3d  %.3f ms/solve" % (cap, st.iterations, a.elapsed_time(b) / n))
 out, st = dco.solve_dense_depth(sysm, cfg, history_cap=0)
-print("default tol: iterations", st.iterations)
+a.record()
+for _ in range(5):
+    out, st = dco.solve_dense_depth(sysm, cfg, history_cap=0)
+b.record()
+torch.cuda.synchronize()
+print("default tol: iterations %d  %.3f ms/solve" % (st.iterations, a.elapsed_time(b) / 5))
