@@ -381,12 +381,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_pcg_tmem(CGArgs a, int chunk, Gr
                 }
             });
             // P1 sums -> per-warp partials in shared memory (frees registers for P2)
+            // recursive halving: 6 double shuffles for the 4 sums instead of 20
+            {
+                double u[4] = {v[1], v[2], v[3], v[4]};
+                warp_halving_reduce<4>(u, lane);
+                if ((lane & 7) == 0) s_w1[warp * 4 + grid_reduce_index<4>(lane)] = u[0];
 #pragma unroll
-            for (int c = 1; c <= 4; ++c) {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], off);
-                if (lane == 0) s_w1[warp * 4 + (c - 1)] = v[c];
-                v[c] = 0.0;
+                for (int c = 1; c <= 4; ++c) v[c] = 0.0;
             }
             tm_wait_st();  // P2 reads rs back
             STAMP(4)
