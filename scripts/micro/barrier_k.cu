@@ -3,6 +3,7 @@
 // burst of global stores before each barrier.
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 namespace cg = cooperative_groups;
 
 #include "../../paper_2203_02300_b200/csrc/grid_reduce.cuh"
@@ -31,6 +32,7 @@ template <int K>
 void run(int stores, GridBar* count, double* part, double* buf, double* sink) {
     int nb = 0;
     cudaDeviceGetAttribute(&nb, cudaDevAttrMultiProcessorCount, 0);
+    if (const char* e = getenv("NB")) nb = atoi(e);  // fewer blocks (e.g. one per cluster of 2)
     int iters = 2000;
     void* params[] = {&iters, &stores, &count, &part, &buf, &sink};
     cudaEvent_t a, b;
