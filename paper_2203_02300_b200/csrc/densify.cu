@@ -1016,15 +1016,33 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         }
     }
     if (kern && !force_big && smem <= kOnchipSmemMax && sms <= 1024) {
+        // Whole blocks where that idles at most 4 SMs: every block then holds
+        // exactly tept * tthreads unknowns and all its slots (config B: 144 x
+        // 6400 = 921,600, five whole rows per block; solve 0.690 -> 0.653 ms
+        // against 148 blocks of 6227). DCO_PCG_PARTIAL=1 keeps one block per SM.
+        int nb = sms, chunk_l = chunk;
+        size_t smem_l = smem;
+        if (!no_tmem && !getenv("DCO_PCG_BLOCKS") && !getenv("DCO_PCG_PARTIAL")) {
+            const long long per = static_cast<long long>(tept) * tthreads;
+            const int nbw = static_cast<int>((static_cast<long long>(n) + per - 1) / per);
+            const int cw = static_cast<int>((n + nbw - 1) / nbw);
+            const size_t sw = (static_cast<size_t>(cw) * 4 + 2 * static_cast<size_t>(w)) * sizeof(double);
+            if (nbw < sms && nbw >= sms - 4 && static_cast<long long>(n / nbw) >= per - tthreads &&
+                sw <= static_cast<size_t>(kOnchipSmemMax)) {
+                nb = nbw;
+                chunk_l = cw;
+                smem_l = sw;
+            }
+        }
         // dynamic shared memory: exactly this launch's need (static scratch
         // comes on top, 227 KB per CTA in total)
-        smem_attr(ctx, kern, static_cast<int>(smem));
-        int chunk_arg = chunk;
+        smem_attr(ctx, kern, static_cast<int>(smem_l));
+        int chunk_arg = chunk_l;
         GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
         cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
         void* params[] = {&a, &chunk_arg, &bar};
-        launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(sms), dim3(tthreads),
-                                      params, smem);
+        launch_cooperative_serialized(ctx, reinterpret_cast<void*>(kern), dim3(nb), dim3(tthreads),
+                                      params, smem_l);
         launched(ctx, no_tmem ? "k_pcg_onchip" : "k_pcg_tmem");
         ctx->last_solver = tthreads != threads ? instance_name("k_pcg_tmem", tept, tthreads)
                                                : instance_name(no_tmem ? "k_pcg_onchip" : "k_pcg_tmem", ept);
