@@ -996,14 +996,16 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     // any-size kernel even when the state fits on chip
     const bool force_stream = getenv("DCO_PCG_FORCE_STREAM") != nullptr;
     const bool force_big = force_stream || getenv("DCO_PCG_FORCE_BIG") != nullptr;
+    // k_pcg_big / k_pcg_share split the unknowns in units of 32 (pcg_big.cuh)
+    const int chunk_a = static_cast<int>(32 * (((n + 31) / 32 + sms - 1) / sms));
     // DCO_PCG_SHARE=1: the co-residency variant (512 threads, p-only shared memory)
     if (getenv("DCO_PCG_SHARE") && sms <= 1024) {
-        const int ept_s = std::max(9, (chunk + kShareThreads - 1) / kShareThreads);
-        const size_t smem_s = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
+        const int ept_s = std::max(9, (chunk_a + kShareThreads - 1) / kShareThreads);
+        const size_t smem_s = (static_cast<size_t>(chunk_a) + 2 * static_cast<size_t>(w)) * sizeof(double);
         BigKernel sk = share_for(ept_s);
         if (sk && smem_s <= kOnchipSmemMax) {
             smem_attr(ctx, sk, static_cast<int>(smem_s));
-            int chunk_arg = chunk;
+            int chunk_arg = chunk_a;
             GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
             cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
             double* hb = static_cast<double*>(scratch(ctx, S_TMP1, 7 * n * sizeof(double)));
@@ -1050,12 +1052,12 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
     }
     // larger frames: p on chip, q/rs in TMEM, r in registers, the rest L2-resident
     {
-        const int ept_b = (chunk + kBigThreads - 1) / kBigThreads;
-        const size_t smem_b = (static_cast<size_t>(chunk) + 2 * static_cast<size_t>(w)) * sizeof(double);
+        const int ept_b = (chunk_a + kBigThreads - 1) / kBigThreads;
+        const size_t smem_b = (static_cast<size_t>(chunk_a) + 2 * static_cast<size_t>(w)) * sizeof(double);
         // 1024 threads (EPT <= 16, 64 TMEM columns per warp) where the chunk
         // fits, else 768 (EPT <= 21): at 1920x1080 3.31 against 3.79 ms
         // (896 threads: 3.46, 640: 4.23). DCO_PCG_BIG768=1 keeps 768.
-        const int ept_k = std::max(8, (chunk + 1023) / 1024);
+        const int ept_k = std::max(8, (chunk_a + 1023) / 1024);
         BigKernel bk = getenv("DCO_PCG_BIG768") ? nullptr : big1024_for(ept_k);
         int bthreads = 1024, e = ept_k;
         if (!bk) {
@@ -1065,7 +1067,7 @@ void solve_dense_dev(dco_ctx* ctx, const dco_system* sys, const dco_config* cfg,
         }
         if (bk && !force_stream && smem_b <= kOnchipSmemMax && sms <= 1024 && !getenv("DCO_PCG_NO_BIG")) {
             smem_attr(ctx, bk, static_cast<int>(smem_b));
-            int chunk_arg = chunk;
+            int chunk_arg = chunk_a;
             GridBar* bar = static_cast<GridBar*>(scratch(ctx, S_RED, sizeof(GridBar)));
             cuda_check(cudaMemsetAsync(bar, 0, sizeof(GridBar), ctx->stream), "memset bar");
             double* hb = static_cast<double*>(scratch(ctx, S_TMP1, 7 * n * sizeof(double)));

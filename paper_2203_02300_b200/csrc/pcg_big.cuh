@@ -39,9 +39,13 @@ __global__ void __launch_bounds__(THREADS, XT ? 2 : 1) k_pcg_big(CGArgs a, int c
     const int w = a.w, h = a.h;
     const int n = static_cast<int>(a.n);
     const int nb = gridDim.x;
-    const int qn = n / nb, rem = n - qn * nb;
-    const int base = blockIdx.x * qn + min(static_cast<int>(blockIdx.x), rem);
-    const int size = qn + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
+    // an even split in units of 32 unknowns: every block starts on a 256 B
+    // boundary, so its rows, halos and the L2-resident vectors stay line-aligned
+    // (the host sizes chunk = 32 * ceil(ceil(n / 32) / nb))
+    const int bi = static_cast<int>(blockIdx.x);
+    const int units = (n + 31) >> 5, qu = units / nb, ru = units - qu * nb;
+    const int base = 32 * (bi * qu + min(bi, ru));
+    const int size = max(0, min(32 * (qu + (bi < ru ? 1 : 0)), n - base));
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int nv = size > t ? (size - t + THREADS - 1) / THREADS : 0;
     double* s_p = sx + w + t;
